@@ -1,0 +1,156 @@
+/*
+ * chp.h -- C ABI of libchp.so, the B200 (sm_100a) implementation of the
+ * Parareal / Cahn-Hilliard hot path of arXiv 2304.14074's reference package
+ * `chparareal` (/root/reference/pkg/src/chparareal).
+ *
+ * The reference is pure Python; its plug-in point for this path is the
+ * propagator interface `propagate(u, spec, steps, stats)` (schemes.py:321-333)
+ * and the four engine call sites that drive it (parareal.py:163, 184, 237,
+ * 248).  Every entry point below replaces one of those, batched over systems
+ * (initial conditions x time slices).  INTEGRATION.md shows the ctypes
+ * binding the Python host layer (paper_2304_14074_b200/_native.py) uses.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers (fp64 unless stated); the caller
+ *    (PyTorch) owns them.  `stream` is a cudaStream_t passed as void*.
+ *  - A field is stored row-major with row pitch `pitch` (>= m) doubles; in 2D
+ *    a field occupies m*pitch doubles, x (i) slow, y (j) fast -- the
+ *    reference's lexicographic order (grid.py:61-67) with padded rows.  The
+ *    pad entries are ignored on input and written as 0 on output.
+ *  - Calls are asynchronous on `stream` unless documented otherwise;
+ *    per-system outcomes are written to a device `chp_sys_info` array.
+ *  - Return codes are chp_status; chp_last_error() gives the message.
+ */
+#ifndef CHP_H_
+#define CHP_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct chp_ctx chp_ctx;
+
+typedef enum {
+  CHP_OK = 0,
+  CHP_ERR_ARG = 1,          /* invalid argument (reference raises ValueError) */
+  CHP_ERR_CUDA = 2,         /* CUDA runtime error */
+  CHP_ERR_UNSUPPORTED = 3   /* grid/scheme combination not implemented */
+} chp_status;
+
+/* Scheme ids -- reference schemes.py:52-58 (NN_LINEAR_A is out of scope). */
+enum { CHP_LINEAR_A = 0, CHP_LINEAR_B = 1, CHP_NONLINEAR_EYRE = 2 };
+
+/* Per-system outcome codes. */
+enum {
+  CHP_SYS_OK = 0,
+  CHP_SYS_NEWTON = 1,     /* NewtonDivergenceError (schemes.py:301-302)      */
+  CHP_SYS_NONFINITE = 2,  /* ValueError non-finite field (grid.py:84-85)     */
+  CHP_SYS_SINGULAR = 3,   /* zero pivot / not SPD (LinearSolveError)          */
+  CHP_SYS_CG = 4          /* 2D CG budget exhausted (LinearSolveError)        */
+};
+
+/* Spatial grid (grid.py:33-67, operator coefficients of grid.py:98-118). */
+typedef struct {
+  int dim;        /* 1 or 2 */
+  int nx;         /* nodes per axis including the boundary */
+  int m;          /* interior points per axis = nx - 2 */
+  int pitch;      /* row pitch in doubles (>= m) */
+  double h;       /* 1/(nx-1) */
+  double hd;      /* h**dim (norm weight, grid.py:149) */
+  double c1;      /* Laplacian off-diagonal 1/h^2 (diagonal -2*dim*c1) */
+  double s_main;  /* 1D bilaplacian interior diagonal (L@L)[i,i] */
+  double s_edge;  /* 1D bilaplacian first/last diagonal */
+  double s_off1;  /* 1D bilaplacian first off-diagonal */
+  double s_off2;  /* 1D bilaplacian second off-diagonal */
+} chp_grid;
+
+/* Propagator spec (schemes.py:61-86); b = eps**2 * dt formed by the caller
+ * exactly as the reference forms it (schemes.py:245, 261, 282). */
+typedef struct {
+  int scheme;
+  int newton_max_iter;
+  double dt;
+  double eps;
+  double b;
+  double newton_tol;
+  double cg_tol;      /* 2D variable-coefficient CG relative tolerance */
+  int cg_max_iter;
+  int pad_;
+} chp_spec;
+
+/* Per-system outcome and Newton aggregates (NewtonStats, schemes.py:100-115). */
+typedef struct {
+  int status;
+  int fail_iter;
+  double fail_resid;
+  long long newton_steps;
+  long long newton_total;
+  int newton_max;
+  int cg_max;
+  double newton_maxres;
+  long long cg_total;
+} chp_sys_info;
+
+const char* chp_version(void);
+const char* chp_status_str(int status);
+
+/* Create a context on `device`: owns cached solver tables (the analogue of
+ * schemes._FACTOR_CACHE, schemes.py:134-142) and scratch.  Not thread safe;
+ * one per device/process. */
+chp_status chp_ctx_create(int device, chp_ctx** out);
+chp_status chp_ctx_destroy(chp_ctx* ctx);
+const char* chp_last_error(chp_ctx* ctx);
+
+/* Zero every chp_sys_info of an array (async). */
+chp_status chp_sysinfo_reset(chp_ctx* ctx, chp_sys_info* info, int n, void* stream);
+
+/*
+ * chp_propagate -- `steps` steps of spec->scheme on `nsys` fields.
+ * Replaces schemes.propagate (schemes.py:321-333) and the step functions
+ * step_linear_a / step_linear_b / step_nonlinear (schemes.py:235-305).
+ * System s reads in + idx(s)*in_stride and writes out + idx(s)*out_stride,
+ * idx(s) = sys_index ? sys_index[s] : s  (sys_index: device int array).
+ * in == out is allowed.  info[idx(s)] accumulates the outcome.
+ */
+chp_status chp_propagate(chp_ctx* ctx, const chp_grid* g, const chp_spec* spec,
+                         int steps, int nsys,
+                         const double* in, long long in_stride,
+                         double* out, long long out_stride,
+                         const int* sys_index, chp_sys_info* info, void* stream);
+
+/*
+ * chp_coarse_sweep -- the sequential coarse recursion of parareal.py:245-251
+ * (mode 1) or the coarse initialisation of parareal.py:182-185 (mode 0), for
+ * `nic` independent initial conditions over slices [n_begin, n_end).
+ *
+ * Layout (per IC i, slice n): U  + i*ic_stride + n*slice_stride  (N+1 slots)
+ *                             F  + i*ic_stride + n*slice_stride  (N slots)
+ *                             G  + i*ic_stride + n*slice_stride  (N slots)
+ * mode 0: U[n+1] = G(U[n]);  G[n] = U[n+1]                   (coarse_init)
+ * mode 1: g = G(U[n]) (reused from G[n] when U[n] is bit-identical to its
+ *         previous value, i.e. changed[n]==0);
+ *         U[n+1] = (g + F[n]) - G[n];  G[n] = g             (parareal.py:249)
+ *         changed[n+1] = any bit of U[n+1] differs; inc[i] = max |dU|.
+ * `changed` (device uint8, nic*(N+1)) must hold changed[i*(N+1)+n_begin] on
+ * entry (1 iff U[n_begin] changed during this sweep).  Bit 1 of
+ * changed[i*(N+1)] (slot 0 -- U[0] never changes) freezes IC i: it is skipped.
+ * `inc` (device double, nic) is max-accumulated.
+ */
+chp_status chp_coarse_sweep(chp_ctx* ctx, const chp_grid* g, const chp_spec* coarse,
+                            int mode, int nic, int nslices, int n_begin, int n_end,
+                            double* U, const double* F, double* G,
+                            long long ic_stride, long long slice_stride,
+                            unsigned char* changed, double* inc,
+                            chp_sys_info* info, void* stream);
+
+/* max |a - b| over n_fields fields of `size` entries (row pitch aware),
+ * max-accumulated into out[0] (device). */
+chp_status chp_max_abs_diff(chp_ctx* ctx, const chp_grid* g, int n_fields,
+                            const double* a, long long a_stride,
+                            const double* b, long long b_stride,
+                            double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHP_H_ */

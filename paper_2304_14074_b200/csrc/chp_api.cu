@@ -1,0 +1,258 @@
+// C ABI of libchp.so (include/chp.h): context, caches, dispatch.
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+
+#include "chp_common.cuh"
+
+// launchers defined in chp_1d.cu / chp_2d.cu / chp_engine.cu
+cudaError_t chp1d_factor(const chp_grid& g, double dt, double b, double* fac, int* err,
+                         cudaStream_t st);
+cudaError_t chp1d_propagate(const chp_grid& g, const chp_spec& sp, int steps, int nsys,
+                            const double* in, long long in_stride, double* out,
+                            long long out_stride, const int* sys_index, const double* fac,
+                            double* ub, double* yh, double* tmp, chp_sys_info* info,
+                            cudaStream_t st);
+cudaError_t chp1d_coarse_sweep(const chp_grid& g, const chp_spec& sp, int mode, int nic, int nsl,
+                               int n0, int n1, double* U, const double* F, double* G,
+                               long long ic_stride, long long sl_stride, unsigned char* changed,
+                               double* inc, const double* fac, double* ub, double* yh,
+                               double* tmp, chp_sys_info* info, cudaStream_t st);
+cudaError_t chp_launch_max_abs_diff(const chp_grid& g, int n_fields, const double* a,
+                                    long long as, const double* b, long long bs, double* out,
+                                    cudaStream_t st);
+struct Chp2d;
+Chp2d* chp2d_create();
+void chp2d_destroy(Chp2d*);
+cudaError_t chp2d_propagate(Chp2d* c, const chp_grid& g, const chp_spec& sp, int steps, int nsys,
+                            const double* in, long long in_stride, double* out,
+                            long long out_stride, const int* sys_index, chp_sys_info* info,
+                            cudaStream_t st, std::string* err);
+cudaError_t chp2d_coarse_sweep(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode,
+                               int nic, int nsl, int n0, int n1, double* U, const double* F,
+                               double* G, long long ic_stride, long long sl_stride,
+                               unsigned char* changed, double* inc, chp_sys_info* info,
+                               cudaStream_t st, std::string* err);
+
+struct chp_ctx {
+  int device = 0;
+  std::string last_error;
+  // cached 1D Cholesky factors keyed by (m, c1, dt, b) -- _FACTOR_CACHE analogue
+  std::map<std::tuple<int, double, double, double>, double*> factors;
+  // grow-only 1D scratch
+  double* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int* dev_err = nullptr;
+  Chp2d* d2 = nullptr;
+};
+
+namespace {
+
+chp_status fail(chp_ctx* c, chp_status s, const std::string& msg) {
+  if (c) c->last_error = msg;
+  return s;
+}
+
+chp_status cuda_fail(chp_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, CHP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool grid_ok(const chp_grid* g, std::string* why) {
+  if (!g) { *why = "null grid"; return false; }
+  if (g->dim != 1 && g->dim != 2) { *why = "dim must be 1 or 2"; return false; }
+  if (g->nx < 4) { *why = "nodes_per_axis must be at least 4"; return false; }
+  if (g->m != g->nx - 2) { *why = "m must equal nx - 2"; return false; }
+  if (g->pitch < g->m) { *why = "pitch must be >= m"; return false; }
+  return true;
+}
+
+bool spec_ok(const chp_spec* s, std::string* why) {
+  if (!s) { *why = "null spec"; return false; }
+  if (s->scheme < CHP_LINEAR_A || s->scheme > CHP_NONLINEAR_EYRE) {
+    *why = "unknown scheme";
+    return false;
+  }
+  if (!(s->dt > 0)) { *why = "dt must be positive"; return false; }
+  if (!(s->eps > 0)) { *why = "eps must be positive"; return false; }
+  if (!(s->newton_tol > 0)) { *why = "newton_tol must be positive"; return false; }
+  if (s->newton_max_iter < 1) { *why = "newton_max_iter must be at least 1"; return false; }
+  return true;
+}
+
+// Scratch for the 1D kernels: ub [m][6][n] + yh [m][n] + tmp [m][n].
+chp_status ensure_scratch(chp_ctx* c, size_t bytes, cudaStream_t st) {
+  if (bytes <= c->scratch_bytes) return CHP_OK;
+  if (c->scratch) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "sync before scratch grow");
+    cudaFree(c->scratch);
+    c->scratch = nullptr;
+    c->scratch_bytes = 0;
+  }
+  cudaError_t e = cudaMalloc(&c->scratch, bytes);
+  if (e != cudaSuccess) return cuda_fail(c, e, "scratch alloc");
+  c->scratch_bytes = bytes;
+  return CHP_OK;
+}
+
+chp_status factor_1d(chp_ctx* c, const chp_grid* g, double dt, double b, cudaStream_t st,
+                     const double** out) {
+  auto key = std::make_tuple(g->m, g->c1, dt, b);
+  auto it = c->factors.find(key);
+  if (it != c->factors.end()) { *out = it->second; return CHP_OK; }
+  double* fac = nullptr;
+  cudaError_t e = cudaMalloc(&fac, sizeof(double) * 3 * g->m);
+  if (e != cudaSuccess) return cuda_fail(c, e, "factor alloc");
+  e = chp1d_factor(*g, dt, b, fac, c->dev_err, st);
+  if (e != cudaSuccess) { cudaFree(fac); return cuda_fail(c, e, "factor launch"); }
+  int herr = 0;
+  e = cudaMemcpyAsync(&herr, c->dev_err, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) { cudaFree(fac); return cuda_fail(c, e, "factor sync"); }
+  if (herr != 0) {
+    cudaFree(fac);
+    char buf[128];
+    snprintf(buf, sizeof buf, "%d-th leading minor not positive definite", herr);
+    return fail(c, CHP_ERR_ARG, buf);
+  }
+  c->factors[key] = fac;
+  *out = fac;
+  return CHP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* chp_version(void) { return "chp-b200 0.1 (sm_100a)"; }
+
+const char* chp_status_str(int s) {
+  switch (s) {
+    case CHP_OK: return "ok";
+    case CHP_ERR_ARG: return "invalid argument";
+    case CHP_ERR_CUDA: return "cuda error";
+    case CHP_ERR_UNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+chp_status chp_ctx_create(int device, chp_ctx** out) {
+  if (!out) return CHP_ERR_ARG;
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return CHP_ERR_CUDA;
+  chp_ctx* c = new chp_ctx();
+  c->device = device;
+  e = cudaMalloc(&c->dev_err, sizeof(int) * 4);
+  if (e != cudaSuccess) { delete c; return CHP_ERR_CUDA; }
+  c->d2 = chp2d_create();
+  *out = c;
+  return CHP_OK;
+}
+
+chp_status chp_ctx_destroy(chp_ctx* c) {
+  if (!c) return CHP_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : c->factors) cudaFree(kv.second);
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->dev_err) cudaFree(c->dev_err);
+  chp2d_destroy(c->d2);
+  delete c;
+  return CHP_OK;
+}
+
+const char* chp_last_error(chp_ctx* c) { return c ? c->last_error.c_str() : "null context"; }
+
+chp_status chp_sysinfo_reset(chp_ctx* c, chp_sys_info* info, int n, void* stream) {
+  if (!info || n < 0) return fail(c, CHP_ERR_ARG, "bad sysinfo array");
+  cudaError_t e = cudaMemsetAsync(info, 0, sizeof(chp_sys_info) * (size_t)n,
+                                  (cudaStream_t)stream);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "sysinfo reset");
+}
+
+chp_status chp_propagate(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int steps, int nsys,
+                         const double* in, long long in_stride, double* out,
+                         long long out_stride, const int* sys_index, chp_sys_info* info,
+                         void* stream) {
+  if (!c) return CHP_ERR_ARG;
+  std::string why;
+  if (!grid_ok(g, &why) || !spec_ok(sp, &why)) return fail(c, CHP_ERR_ARG, why);
+  if (steps < 1) return fail(c, CHP_ERR_ARG, "steps must be at least 1");
+  if (nsys < 0 || !in || !out || !info) return fail(c, CHP_ERR_ARG, "bad arrays");
+  if (nsys == 0) return CHP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g->dim == 1) {
+    const double* fac = nullptr;
+    if (sp->scheme == CHP_LINEAR_B) {
+      chp_status s = factor_1d(c, g, sp->dt, sp->b, st, &fac);
+      if (s != CHP_OK) return s;
+    }
+    const size_t per = (size_t)g->m * (size_t)nsys * sizeof(double);
+    chp_status s = ensure_scratch(c, per * 8, st);
+    if (s != CHP_OK) return s;
+    double* ub = c->scratch;
+    double* yh = ub + (size_t)g->m * 6 * nsys;
+    double* tmp = yh + (size_t)g->m * nsys;
+    cudaError_t e = chp1d_propagate(*g, *sp, steps, nsys, in, in_stride, out, out_stride,
+                                    sys_index, fac, ub, yh, tmp, info, st);
+    return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp1d_propagate");
+  }
+  cudaError_t e = chp2d_propagate(c->d2, *g, *sp, steps, nsys, in, in_stride, out, out_stride,
+                                  sys_index, info, st, &why);
+  if (!why.empty()) return fail(c, CHP_ERR_UNSUPPORTED, why);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp2d_propagate");
+}
+
+chp_status chp_coarse_sweep(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int mode, int nic,
+                            int nsl, int n0, int n1, double* U, const double* F, double* G,
+                            long long ic_stride, long long sl_stride, unsigned char* changed,
+                            double* inc, chp_sys_info* info, void* stream) {
+  if (!c) return CHP_ERR_ARG;
+  std::string why;
+  if (!grid_ok(g, &why) || !spec_ok(sp, &why)) return fail(c, CHP_ERR_ARG, why);
+  if (mode != 0 && mode != 1) return fail(c, CHP_ERR_ARG, "mode must be 0 or 1");
+  if (nic < 1 || nsl < 1 || n0 < 0 || n1 > nsl || n0 > n1)
+    return fail(c, CHP_ERR_ARG, "bad slice range");
+  if (!U || !G || !info || (mode == 1 && (!F || !changed)))
+    return fail(c, CHP_ERR_ARG, "bad arrays");
+  if (n0 == n1) return CHP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g->dim == 1) {
+    const double* fac = nullptr;
+    if (sp->scheme == CHP_LINEAR_B) {
+      chp_status s = factor_1d(c, g, sp->dt, sp->b, st, &fac);
+      if (s != CHP_OK) return s;
+    }
+    const size_t per = (size_t)g->m * (size_t)nic * sizeof(double);
+    chp_status s = ensure_scratch(c, per * 8, st);
+    if (s != CHP_OK) return s;
+    double* ub = c->scratch;
+    double* yh = ub + (size_t)g->m * 6 * nic;
+    double* tmp = yh + (size_t)g->m * nic;
+    cudaError_t e = chp1d_coarse_sweep(*g, *sp, mode, nic, nsl, n0, n1, U, F, G, ic_stride,
+                                       sl_stride, changed, inc, fac, ub, yh, tmp, info, st);
+    return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp1d_coarse_sweep");
+  }
+  cudaError_t e = chp2d_coarse_sweep(c->d2, *g, *sp, mode, nic, nsl, n0, n1, U, F, G, ic_stride,
+                                     sl_stride, changed, inc, info, st, &why);
+  if (!why.empty()) return fail(c, CHP_ERR_UNSUPPORTED, why);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp2d_coarse_sweep");
+}
+
+chp_status chp_max_abs_diff(chp_ctx* c, const chp_grid* g, int n_fields, const double* a,
+                            long long as, const double* b, long long bs, double* out,
+                            void* stream) {
+  if (!c) return CHP_ERR_ARG;
+  std::string why;
+  if (!grid_ok(g, &why)) return fail(c, CHP_ERR_ARG, why);
+  if (n_fields < 0 || !a || !b || !out) return fail(c, CHP_ERR_ARG, "bad arrays");
+  if (n_fields == 0) return CHP_OK;
+  cudaError_t e = chp_launch_max_abs_diff(*g, n_fields, a, as, b, bs, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "max_abs_diff");
+}
+
+}  // extern "C"
