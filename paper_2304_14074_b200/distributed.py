@@ -1,0 +1,166 @@
+"""Multi-GPU Parareal: time slices sharded contiguously over ranks.
+
+Rank r of P owns slices [r*N/P, (r+1)*N/P).  Per iteration:
+
+1. fine sweep over the rank's changed slices -- no communication;
+2. coarse sweep as a chain: rank r receives U_{s0}^{k+1} (plus its
+   "changed in this sweep" flag) from rank r-1, runs its coarse steps +
+   corrections on the device, and sends U_{s1}^{k+1} to rank r+1
+   (torch.distributed send/recv over NCCL / NVLink; one field per hop);
+3. the increment max_{n,i} |dU| is an all-reduce(max) of one double.
+
+The chain adds no arithmetic, so iterates are bit-identical for any P.
+The local engine only needs the small interface used below, so the chain
+logic is testable on CPU with gloo and a host engine (tests/test_distributed.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard(N: int, world: int, rank: int) -> tuple[int, int]:
+    if N % world:
+        raise ValueError(f"{N} slices do not shard evenly over {world} ranks")
+    L = N // world
+    return rank * L, (rank + 1) * L
+
+
+class ShardedParareal:
+    def __init__(self, grid, fine, coarse, num_slices: int, fine_steps: int, *, rank: int = 0,
+                 world: int = 1, engine_factory=None, inc_tol: float = 1e-10, device=None):
+        import torch
+        self.rank, self.world = rank, world
+        self.N, self.J = num_slices, fine_steps
+        self.s0, self.s1 = shard(num_slices, world, rank)
+        self.local_slices = self.s1 - self.s0
+        if engine_factory is None:
+            from .engine import PararealEngine
+            engine_factory = PararealEngine
+        self.eng = engine_factory(grid, fine, coarse, self.local_slices, fine_steps, batch=1,
+                                  device=device)
+        self.grid = grid
+        self.inc_tol = inc_tol
+        self.k = 0
+        self.converged_at = None
+        self.increments = []
+        self._torch = torch
+
+    # -- communication helpers ------------------------------------------------
+    def _dist(self):
+        import torch.distributed as dist
+        return dist
+
+    def _recv_boundary(self):
+        """U_{s0} and its changed flag from rank-1 into local slot 0."""
+        if self.rank == 0:
+            return
+        dist = self._dist()
+        dist.recv(self.eng.U[0, 0], src=self.rank - 1)
+        flag = self._torch.zeros(1, dtype=self._torch.uint8, device=self.eng.U.device)
+        dist.recv(flag, src=self.rank - 1)
+        self.eng.changed[0, 0] = flag[0]
+
+    def _send_boundary(self):
+        if self.rank == self.world - 1:
+            return
+        dist = self._dist()
+        L = self.local_slices
+        dist.send(self.eng.U[0, L].contiguous(), dst=self.rank + 1)
+        flag = self.eng.changed[0, L:L + 1].clone()
+        dist.send(flag, dst=self.rank + 1)
+
+    # -- phases ---------------------------------------------------------------
+    def load(self, u0) -> None:
+        if self.rank == 0:
+            self.eng.load([u0])
+
+    def coarse_init(self) -> None:
+        self._recv_boundary()
+        self.eng.coarse_range(0, 0, self.local_slices)
+        self._send_boundary()
+        self.eng.changed.fill_(1)        # every F(U_n^0) is needed at k = 0
+        self.k = 0
+
+    def iterate(self, force_all: bool = False) -> float:
+        eng = self.eng
+        flags = eng.changed.cpu().numpy()
+        if force_all:
+            flags[:, : self.local_slices] |= 1
+        eng.fine_sweep(flags)
+        eng.inc.zero_()
+        self._recv_boundary()
+        if self.rank == 0:
+            eng.changed[0, 0] = 1 if force_all else 0
+        elif force_all:
+            eng.changed[0, 0] = 1
+        eng.coarse_range(1, 0, self.local_slices)
+        self._send_boundary()
+        eng.check_status()
+        inc = eng.inc.clone()
+        if self.world > 1:
+            self._dist().all_reduce(inc, op=self._dist().ReduceOp.MAX)
+        val = float(inc[0])
+        self.k += 1
+        self.increments.append(val)
+        if self.converged_at is None and val < self.inc_tol:
+            self.converged_at = self.k
+        return val
+
+    def run(self, max_iter: int | None = None):
+        if max_iter is None:
+            max_iter = self.N + 2
+        self.coarse_init()
+        while self.converged_at is None and self.k < max_iter:
+            self.iterate()
+        return self.converged_at
+
+    def local_iterates(self) -> np.ndarray:
+        """Host copy of U_{s0+1} .. U_{s1} (and U_0 on rank 0)."""
+        U = self.eng.iterates_host(0)
+        return U if self.rank == 0 else U[1:]
+
+    # -- measurement helpers (bench.py) ----------------------------------------
+    def time_fine_sweep(self) -> float:
+        """Device time (ms) of one fine sweep over every local slice."""
+        torch = self._torch
+        flags = np.ones((1, self.local_slices + 1), dtype=np.uint8)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        self.eng.fine_sweep(flags)
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
+    def e2e_step_rate(self, steps: int) -> dict:
+        """Same metric with host-resident iterates: per step the local iterates
+        and coarse values are copied H2D from pinned memory, one forced
+        iteration runs, and the new iterates are copied back D2H."""
+        torch = self._torch
+        eng = self.eng
+        hU = torch.empty(eng.U.shape, dtype=torch.float64, pin_memory=True)
+        hG = torch.empty(eng.G.shape, dtype=torch.float64, pin_memory=True)
+        hU.copy_(eng.U)
+        hG.copy_(eng.G)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            eng.U.copy_(hU, non_blocking=True)
+            eng.G.copy_(hG, non_blocking=True)
+            self.iterate(force_all=True)
+            hU.copy_(eng.U, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        if self.world > 1:
+            t = torch.tensor([ms], device=eng.U.device, dtype=torch.float64)
+            self._dist().all_reduce(t, op=self._dist().ReduceOp.MAX)
+            ms = float(t.item())
+        pts = self.N * self.J * self.grid.interior_count
+        nbytes = eng.U.numel() * 8
+        return {"value": pts / (ms * 1e-3), "unit": "grid-point-steps/s",
+                "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": nbytes,
+                "ms_per_step": ms,
+                "path": "pinned host iterates -> engine (chp_propagate/chp_coarse_sweep) -> host"}

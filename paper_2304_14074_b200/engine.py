@@ -111,6 +111,10 @@ class PararealEngine:
         m = self.grid.interior_per_axis
         return (m,) if self.grid.dim == 1 else (m, self.grid.pitch)
 
+    def coarse_range(self, mode: int, n0: int, n1: int):
+        """chp_coarse_sweep over local slices [n0, n1) (no host sync)."""
+        self._coarse(mode, n0, n1)
+
     def _coarse(self, mode: int, n0: int, n1: int):
         st = self.ctx.L.chp_coarse_sweep(
             self.ctx.h, self._native_grid(), self.coarse.native(), mode, self.B, self.N, n0, n1,
@@ -197,6 +201,18 @@ class PararealEngine:
             self.converged_at[i] = self.k
             self.changed[i, 0] |= 2
         return inc
+
+    def check_status(self) -> None:
+        """Raise the reference exception for any failed fine/coarse system and
+        fold Newton aggregates into ``self.newton`` (one host sync)."""
+        si = self._raise(self.info_fine, self.fine)
+        if self.fine.scheme is Scheme.NONLINEAR_EYRE:
+            self.newton.absorb(si)
+        self.info_fine.zero_()
+        sc = self._raise(self.info_coarse, self.coarse)
+        if self.coarse.scheme is Scheme.NONLINEAR_EYRE:
+            self.newton.absorb(sc)
+        self.info_coarse.zero_()
 
     def run(self, max_iter: int | None = None, on_iteration=None) -> list:
         """Coarse init + iterate until every IC's increment < inc_tol."""

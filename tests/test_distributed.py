@@ -1,0 +1,110 @@
+"""Sharded (multi-rank) Parareal chain logic on CPU: world_size 2 over gloo.
+
+The device engine is swapped for a host engine that implements the same
+interface with the CPU oracle's propagators (test infrastructure), so the
+send/recv chain, the changed-flag hand-off and the all-reduce of the increment
+are exercised without a GPU.  Iterates must be bit-identical to the
+single-process oracle run, with the same iteration count.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import chp_oracle as O
+
+KN = O.Knobs(cube="exact")
+_SCHEME = {"linear-a": O.LINEAR_A, "linear-b": O.LINEAR_B, "nonlinear-eyre": O.EYRE}
+
+
+class HostEngine:
+    """CPU stand-in for engine.PararealEngine (same attributes / semantics)."""
+
+    def __init__(self, grid, fine, coarse, L, J, batch=1, device=None):
+        self.mesh = O.Mesh(grid.dim, grid.nodes_per_axis)
+        self.fine, self.coarse, self.L, self.J = fine, coarse, L, J
+        n = self.mesh.size
+        self.U = torch.zeros((1, L + 1, n), dtype=torch.float64)
+        self.G = torch.zeros_like(self.U)
+        self.F = torch.zeros_like(self.U)
+        self.changed = torch.zeros((1, L + 1), dtype=torch.uint8)
+        self.inc = torch.zeros(1, dtype=torch.float64)
+
+    def _step(self, spec, v, steps):
+        return O.advance(self.mesh, v, _SCHEME[spec.scheme.value], spec.dt, spec.eps, steps, KN)
+
+    def load(self, u0s):
+        self.U[0, 0] = torch.as_tensor(u0s[0].values)
+
+    def fine_sweep(self, flags):
+        for n in range(self.L):
+            if flags[0, n] & 1:
+                self.F[0, n] = torch.as_tensor(self._step(self.fine, self.U[0, n].numpy(), self.J))
+
+    def coarse_range(self, mode, n0, n1):
+        U, G, F, ch = self.U[0].numpy(), self.G[0].numpy(), self.F[0].numpy(), self.changed[0]
+        for n in range(n0, n1):
+            if mode == 0:
+                U[n + 1] = self._step(self.coarse, U[n], 1)
+                G[n] = U[n + 1]
+                continue
+            g = self._step(self.coarse, U[n], 1) if ch[n] & 1 else G[n].copy()
+            new = (g + F[n]) - G[n]
+            ch[n + 1] = int(not np.array_equal(new.view(np.int64), U[n + 1].view(np.int64)))
+            self.inc[0] = max(float(self.inc[0]), float(np.max(np.abs(new - U[n + 1]))))
+            U[n + 1] = new
+            G[n] = g
+
+    def check_status(self):
+        pass
+
+    def iterates_host(self, i):
+        return self.U[i].numpy().copy()
+
+
+def _worker(rank, world, port, var, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2304_14074_b200 import parareal as P
+    from paper_2304_14074_b200.distributed import ShardedParareal
+    from paper_2304_14074_b200.grid import Field, SpatialGrid
+    g = SpatialGrid(1, 17)
+    part = P.TimePartition(0.05, 4, 4)
+    f, c = P.propagator_pair(P.AlgorithmVariant(var), part, 0.1)
+    sh = ShardedParareal(g, f, c, 4, 4, rank=rank, world=world, engine_factory=HostEngine)
+    u0 = np.random.default_rng(3).uniform(-0.5, 0.5, 15)
+    sh.load(Field(g, u0))
+    k = sh.run()
+    out_q.put((rank, k, sh.increments, sh.local_iterates()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("var", ["pa3", "npa1"])
+def test_two_rank_chain_bit_identical(var):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, var, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    u0 = np.random.default_rng(3).uniform(-0.5, 0.5, 15)
+    ref = O.parareal(O.Mesh(1, 17), u0, var, 0.05, 4, 4, 0.1, KN)
+    assert res[0][1] == res[1][1] == ref.k
+    assert np.array_equal(np.array(res[0][2]), np.array(ref.increments))
+    U = np.concatenate([res[0][3], res[1][3]])
+    assert np.array_equal(U, ref.iterates)
+
+
+def test_shard_bounds():
+    from paper_2304_14074_b200.distributed import shard
+    assert shard(512, 8, 3) == (192, 256)
+    with pytest.raises(ValueError):
+        shard(10, 4, 0)
