@@ -53,7 +53,7 @@ SYSINFO_DTYPE = np.dtype([("status", np.int32), ("fail_iter", np.int32),
                           ("cg_total", np.int64)])
 assert SYSINFO_DTYPE.itemsize == C.sizeof(ChpSysInfo) == 56
 
-_lock = threading.Lock()
+_lock = threading.RLock()
 _lib = None
 
 

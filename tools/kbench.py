@@ -1,0 +1,80 @@
+"""Kernel micro-timings on the GPU (CUDA events): 2D LINEAR_B fine propagator,
+2D LINEAR_A PCG coarse step, 1D propagators.  Usage: python tools/kbench.py [what]"""
+import json
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2304_14074_b200 import schemes as S  # noqa: E402
+from paper_2304_14074_b200.grid import SpatialGrid, to_device_layout  # noqa: E402
+
+
+def ev_time(fn, reps=3):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def fields(g, n, seed=0, base=0.0):
+    rng = np.random.default_rng(seed)
+    flat = torch.tensor(base + rng.uniform(-0.05, 0.05, (n, g.interior_count)), device="cuda")
+    return torch.stack([to_device_layout(g, flat[i]) for i in range(n)])
+
+
+def linb_2d(nx=1025, nsys=64, steps=16):
+    g = SpatialGrid(2, nx)
+    src = fields(g, nsys, base=0.1)
+    out = torch.empty_like(src)
+    spec = S.PropagatorSpec(S.Scheme.LINEAR_B, 2.0 / 512 / 256, 0.01)
+    ms = ev_time(lambda: S.propagate_batch(g, spec, steps, src, out))
+    pts = nsys * steps * g.interior_count
+    return {"what": "2D LINEAR_B", "nx": nx, "nsys": nsys, "steps": steps, "ms": ms,
+            "pt_steps_per_s": pts / (ms * 1e-3), "GBps_at_32B": 32 * pts / (ms * 1e-3) / 1e9}
+
+
+def lina_2d(nx=1025, nsys=1):
+    g = SpatialGrid(2, nx)
+    src = fields(g, nsys, base=0.1)
+    out = torch.empty_like(src)
+    spec = S.PropagatorSpec(S.Scheme.LINEAR_A, 2.0 / 512, 0.01)
+    info = S.new_sysinfo(nsys, "cuda")
+    ms = ev_time(lambda: S.propagate_batch(g, spec, 1, src, out, info=info), reps=3)
+    si = S.read_sysinfo(info)
+    return {"what": "2D LINEAR_A PCG", "nx": nx, "nsys": nsys, "ms": ms,
+            "cg_iters": int(si["cg_total"][0]) / 4}
+
+
+def one_d(nx, nsys, scheme, dt, eps, steps):
+    g = SpatialGrid(1, nx)
+    src = torch.tensor(np.random.default_rng(0).uniform(-0.05, 0.05, (nsys, nx - 2)), device="cuda")
+    out = torch.empty_like(src)
+    spec = S.PropagatorSpec(scheme, dt, eps)
+    ms = ev_time(lambda: S.propagate_batch(g, spec, steps, src, out), reps=2)
+    pts = nsys * steps * (nx - 2)
+    return {"what": f"1D {scheme.value}", "nx": nx, "nsys": nsys, "steps": steps, "ms": ms,
+            "pt_steps_per_s": pts / (ms * 1e-3)}
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    res = []
+    if what in ("all", "2d"):
+        res.append(linb_2d(1025, 64, 16))
+        res.append(linb_2d(257, 64, 64))
+        res.append(lina_2d(1025, 1))
+        res.append(lina_2d(257, 1))
+    if what in ("all", "1d"):
+        res.append(one_d(257, 16, S.Scheme.LINEAR_B, 2.0 ** -12, 0.05, 256))
+        res.append(one_d(1025, 4096, S.Scheme.NONLINEAR_EYRE, 2.0 ** -15, 0.03, 16))
+        res.append(one_d(1025, 64, S.Scheme.LINEAR_A, 2.0 ** -5, 0.03, 1))
+    for r in res:
+        print(json.dumps(r), flush=True)
