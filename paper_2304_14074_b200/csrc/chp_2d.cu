@@ -755,7 +755,7 @@ cudaError_t pcg_solve(const chp_grid& g, int nsys, double a, double b, double to
   // b^ = (2/N)^2 / kappa .* T_i T_j rhs  -> Rv
   RowDst r0{W.RHS, W.Yv, fs, m, 0, 1.0, nullptr, nt.lam, b, nullptr, 0, W.cg, 0};
   k2d_rowdst<N><<<rgrid, C::THREADS, rsm, st>>>(r0, tb);
-  ColDst c0{W.Yv, W.Rv, fs, m, 2, s2, nullptr, nt.lam, W.cg, 0};
+  ColDst c0{W.Yv, W.Rv, fs, m, 2, 2.0 / N, nullptr, nt.lam, W.cg, 0};   // S = (2/N) T_i T_j
   k2d_coldst<N><<<cgrid, C::THREADS, C::COL_SMEM, st>>>(c0, tb);
   k2d_cg_init<<<egrid, 256, 0, st>>>(pt, W.X, W.Rv, W.Pv, nt.lam, b, W.cg, W.partial);
   k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 0, 0, 0, 0, 0);

@@ -60,7 +60,9 @@ def test_single_steps_bitwise_vs_oracle(P, golden):
                 got = S.propagate(G.Field(g, v), spec, steps).values
                 assert np.array_equal(got, want), (ci, s, steps, rel(got, want))
                 if f"{s}{steps}_{ci}" in z:   # unmodified reference (numpy cube)
-                    assert rel(got, z[f"{s}{steps}_{ci}"]) < 1e-12, (ci, s, steps)
+                    # only the host's numpy v**3 (1-ulp, SVML) differs; Newton amplifies it
+                    tol = 1e-12 if s != "n" else 1e-10
+                    assert rel(got, z[f"{s}{steps}_{ci}"]) < tol, (ci, s, steps)
 
 
 def test_batched_propagate_with_index(P):
@@ -177,12 +179,18 @@ def test_config1_iterates_vs_reference(P, golden):
     eng = PararealEngine(g, f, c, 16, 256)
     eng.load([G.Field(g, z["u0"])])
     eng.coarse_init()
+    ref = O.parareal(O.Mesh(1, 257), z["u0"], "pa3", 1.0, 16, 256, 0.05, EXACT,
+                     keep_history=True)
     for k in range(1, 18):
         eng.iterate()
+        assert np.array_equal(eng.iterates_host(), ref.history[k - 1])   # bit-identical
+        # Intermediate iterates pass through the kappa~1e7 coarse solve, which
+        # amplifies the reference host's 1-ulp v**3 differences (SURVEY.md 8(c),
+        # T2 note); converged iterates are insensitive.
         if k == 1:
             assert rel(eng.iterates_host(), z["pa3_U1"]) < 1e-10
         if k == 8:
-            assert rel(eng.iterates_host(), z["pa3_U8"]) < 1e-10
+            assert rel(eng.iterates_host(), z["pa3_U8"]) < 1e-8
     U = eng.iterates_host()
     assert rel(U, z["pa3_U"]) < 1e-10
     assert eng.converged_at[0] == 17
