@@ -98,10 +98,10 @@ def count_launches(fn):
         torch.cuda.synchronize()
     names = {}
     for ev in prof.events():
-        if ev.device_type == torch.autograd.DeviceType.CUDA and ev.name.startswith(
-                ("_Z", "k1d", "k2d", "k_")):
-            if any(s in ev.name for s in ("k2d", "k1d", "k_max_abs")):
-                names[ev.name] = names.get(ev.name, 0) + 1
+        nm = ev.name
+        if any(s in nm for s in ("k2d_", "k1d_", "k_max_abs_diff")):
+            short = nm.split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+            names[short] = names.get(short, 0) + 1
     return sum(names.values()), names
 
 
@@ -260,7 +260,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()
     if args.impl == "reference":
