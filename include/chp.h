@@ -13,10 +13,11 @@
  * Conventions
  *  - All array pointers are DEVICE pointers (fp64 unless stated); the caller
  *    (PyTorch) owns them.  `stream` is a cudaStream_t passed as void*.
- *  - A field is stored row-major with row pitch `pitch` (>= m) doubles; in 2D
- *    a field occupies m*pitch doubles, x (i) slow, y (j) fast -- the
- *    reference's lexicographic order (grid.py:61-67) with padded rows.  The
- *    pad entries are ignored on input and written as 0 on output.
+ *  - A 1D field is m contiguous doubles.  A 2D field is m rows of pitch
+ *    N = m+1 doubles, x (i) slow, y (j) fast -- the reference's lexicographic
+ *    order (grid.py:61-67) -- each row laid out [0, v_1, ..., v_m]: column 0
+ *    is the zero Dirichlet boundary, so storage index = math index and rows
+ *    are 16-byte aligned.  The pad is ignored on input, written 0 on output.
  *  - Calls are asynchronous on `stream` unless documented otherwise;
  *    per-system outcomes are written to a device `chp_sys_info` array.
  *  - Return codes are chp_status; chp_last_error() gives the message.

@@ -1,18 +1,23 @@
 // 2D propagators (configs 3-5): batched DST-I spectral solves.
 //
-// Field layout: [m rows (x, i)][pitch = N = m+1 doubles (y, j)], N a power of
-// two; column j = m is a zero pad.  All transforms are the unnormalised DST-I
-// T (T^2 = (N/2) I) of chp_dst.cuh; the 2D orthonormal transform is
-// S = (2/N) T_i T_j, so every normalisation folds into one scale per solve.
+// Field layout: [m rows (x, i)][pitch N = m+1 doubles (y, j)], N a power of
+// two.  Storage column j holds math index j: column 0 is the zero Dirichlet
+// pad, columns 1..m the interior -- so the pair (2k, 2k+1) of a row is one
+// aligned double2.  All transforms are unnormalised DST-I (T^2 = (N/2) I,
+// chp_wdst.cuh); the orthonormal 2D transform is S = (2/N) T_i T_j and every
+// normalisation folds into one scale per solve.
 //
 // LINEAR_B (schemes.py:249-267):  x = S D S rhs,  D = 1/(1 - 2dt lam + eps^2 dt lam^2),
-// lam = lam_p + lam_q (grid.py:127-144, sin^2 form).  One step = two passes
-// over HBM (32 B per grid-point-step):
-//   row pass    (contiguous rows, tile of TR rows + 1 halo row each side):
-//               P -> x = T_j P (physical), rhs = x + dt L(x^3 - 3x) (5-point,
-//               CSR order of grid.py:110), Q = T_j rhs
-//   column pass (tile of TC columns, all rows): P = T_i (D' .* (T_i Q))
-// with D' = (2/N)^2 D.  J steps = J+1 row passes + J column passes.
+// lam = lam_p + lam_q (grid.py:127-144 eigenvalues in the sin^2 form).
+// One step = two passes over HBM (32 B per grid-point-step):
+//   row pass    (tile of TR rows + 1 halo row on each side; one lane group
+//                per row pair):  x = T_j P (registers) -> w = x^3 - 3x (SMEM)
+//                -> Q = (N/2) P + dt T_j(L w)      [T_j x = (N/2) P exactly]
+//                (first step: Q = T_j(x + dt L w) from the physical input)
+//   column pass (tile of TC columns, all rows, one lane group per column pair):
+//                P = T_i (D' .* T_i Q),  D' = (2/N)^2 D
+// J steps = J+1 row passes + J column passes, every slice of every IC in
+// each launch.
 #include <math.h>
 
 #include <map>
@@ -21,6 +26,7 @@
 
 #include "chp_common.cuh"
 #include "chp_dst.cuh"
+#include "chp_wdst.cuh"
 
 using chpdst::Tables;
 
@@ -29,15 +35,26 @@ namespace {
 constexpr int kMinN = 8;
 constexpr int kMaxN = 1024;
 
+// configuration of the smem (radix-4 Stockham) passes used by the PCG
 template <int N> struct Cfg {
   static constexpr int T = (N >= 1024) ? 128 : (N >= 512 ? 64 : 32);  // threads / pair
   static constexpr int G = 4;                                          // pairs / block
-  static constexpr int TR = 2 * G - 2;                                 // rows / row tile
   static constexpr int TC = 2 * G;                                     // cols / col tile
   static constexpr int THREADS = G * T;
-  static constexpr size_t ROW_SMEM = sizeof(double) * ((size_t)(TR + 2) * N + (size_t)TR * N) +
-                                     sizeof(double) * G * (T / 32);
   static constexpr size_t COL_SMEM = sizeof(double) * (size_t)TC * N + sizeof(double) * G * (T / 32);
+};
+
+// configuration of the register-resident (wdst) LINEAR_B passes
+template <int N> struct WCfg {
+  static constexpr int L = wdst::Geo<N>::L;
+  static constexpr int WARPS = (N >= 64) ? 8 : 1;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int GPB = THREADS / L;          // lane groups (pairs) per block
+  static constexpr int ROWS = 2 * GPB;             // rows held per row tile (incl. halo)
+  static constexpr int TR = ROWS - 2;              // inner rows per row tile
+  static constexpr int TC = (2 * GPB < N) ? 2 * GPB : N;   // columns per column tile
+  static constexpr size_t ROW_SMEM = sizeof(double) * (size_t)ROWS * N + 16 * (size_t)N;
+  static constexpr size_t COL_SMEM = sizeof(double) * (size_t)(2 * GPB) * N + 16 * (size_t)N;
 };
 
 enum RowMode { ROW_FIRST = 0, ROW_MID = 1, ROW_LAST = 2 };
@@ -52,100 +69,151 @@ struct RowArgs {
   int m;
   double dt, c1;
   int mode;
-  chp_sys_info* info;    // indexed like `in_index`/`out_index` of the physical side
+  chp_sys_info* info;    // per-system outcome, indexed through info_index
   const int* info_index;
+  const double2* wtab;   // wdst lane tables for N
 };
 
+CHP_DEV double w_of(double x) { return fma(x, x * x, -3.0 * x); }   // x^3 - 3x
+
 // ---------------------------------------------------------------------------
-// Row pass
+// LINEAR_B row pass
 // ---------------------------------------------------------------------------
 template <int N>
-__global__ void __launch_bounds__(Cfg<N>::THREADS)
-k2d_row_pass(RowArgs a, Tables tb) {
-  using C = Cfg<N>;
-  extern __shared__ double sm[];
-  double* X = sm;                                // (TR+2) rows, pairs of 2N
-  double* R = sm + (size_t)(C::TR + 2) * N;      // TR rows
-  double* ws = R + (size_t)C::TR * N;
+__global__ void __launch_bounds__(WCfg<N>::THREADS)
+k2d_row_pass(RowArgs a) {
+  using C = WCfg<N>;
+  constexpr int L = C::L;
+  extern __shared__ __align__(16) double sm[];   // ROWS rows of N (swizzled rsw) + twiddles
+  double2* twt = reinterpret_cast<double2*>(sm + (size_t)C::ROWS * N);
   const int tid = threadIdx.x;
-  const int g = tid / C::T, t = tid % C::T;
+  const int g = tid / L, l = tid % L;
   const int s = blockIdx.y;
   const int m = a.m;
-  const int i0 = blockIdx.x * C::TR;
+  const int i0 = blockIdx.x * C::TR;              // first inner row of the tile
   const long long fin = a.in_index ? a.in_index[s] : s;
   const long long fout = a.out_index ? a.out_index[s] : s;
-  const double* in = a.in + fin * a.in_stride;
-  double* out = a.out + fout * a.out_stride;
-
-  // 1. load rows i0-1 .. i0+TR (zero outside), math index j+1
-  for (int idx = tid; idx < (C::TR + 2) * N; idx += C::THREADS) {
-    const int r = idx / N, j = idx % N;
-    const int row = i0 - 1 + r;
-    double v = 0.0;
-    if (j > 0 && row >= 0 && row < m) v = in[(long long)row * N + (j - 1)];
-    X[idx] = v;
-  }
+  const double* __restrict__ in = a.in + fin * a.in_stride;
+  double* __restrict__ out = a.out + fout * a.out_stride;
+  wdst::load_twiddles<N>(twt, a.wtab + N);
+  const double2 ac = __ldg(&a.wtab[l]);
+  double* wr0 = sm + (size_t)(2 * g) * N;         // this group's two tile rows
+  double* wr1 = wr0 + N;
+  double2* scr = reinterpret_cast<double2*>(wr0);
+  const int ga = i0 - 1 + 2 * g, gb = ga + 1;     // their global rows
+  const bool va = ga >= 0 && ga < m, vb = gb >= 0 && gb < m;
+  const double* pa = in + (long long)(va ? ga : 0) * N;
+  const double* pb = in + (long long)(vb ? gb : 0) * N;
   __syncthreads();
-  // 2. x = T_j P
-  if (a.mode != ROW_FIRST) {
-    chpdst::dst_pair<N, C::T>(X + (size_t)g * 2 * N, tb, 1.0, ws + g * (C::T / 32), t, g + 1);
-    __syncthreads();
-    // non-finite check of the physical state (grid.py:84-85, every step)
-    bool bad = false;
-    for (int idx = tid; idx < C::TR * N; idx += C::THREADS) {
-      const int r = idx / N, j = idx % N;
-      if (i0 + r < m && j > 0) bad |= !isfinite(X[(size_t)(r + 1) * N + j]);
+
+  // -- phase 1: x of tile rows (2g, 2g+1) -> w = x^3 - 3x in SMEM ---------------
+  if (a.mode == ROW_FIRST) {
+    for (int j = l; j < N; j += L) {
+      wr0[wdst::rsw(j)] = va ? w_of(pa[j]) : 0.0;
+      wr1[wdst::rsw(j)] = vb ? w_of(pb[j]) : 0.0;
     }
+  } else {
+    const bool last = a.mode == ROW_LAST;
+    const bool ina = va && ga >= i0 && ga < i0 + C::TR;   // only inner rows are output
+    const bool inb = vb && gb >= i0 && gb < i0 + C::TR;
+    bool bad = false;
+    auto ld = [&](int n, double& x, double& xm, double& y, double& ym) {
+      const bool z0 = (n == 0);
+      x = (va && !z0) ? pa[n] : 0.0;
+      xm = (va && !z0) ? pa[N - n] : 0.0;
+      y = (vb && !z0) ? pb[n] : 0.0;
+      ym = (vb && !z0) ? pb[N - n] : 0.0;
+    };
+    auto st = [&](int k, double a2, double a21, double b2, double b21) {
+      bad |= (ina && !(isfinite(a2) && isfinite(a21))) || (inb && !(isfinite(b2) && isfinite(b21)));
+      if (last) {
+        if (ina) *reinterpret_cast<double2*>(out + (long long)ga * N + 2 * k) = make_double2(a2, a21);
+        if (inb) *reinterpret_cast<double2*>(out + (long long)gb * N + 2 * k) = make_double2(b2, b21);
+      } else {
+        *reinterpret_cast<double2*>(wr0 + wdst::rsw(2 * k)) = make_double2(w_of(a2), w_of(a21));
+        *reinterpret_cast<double2*>(wr1 + wdst::rsw(2 * k)) = make_double2(w_of(b2), w_of(b21));
+      }
+    };
+    wdst::pair_dst<N>(ld, st, scr, twt, l, ac);
     if (__syncthreads_or(bad) && tid == 0) {
       const long long fi = a.info_index ? a.info_index[s] : s;
       atomicCAS(&a.info[fi].status, CHP_SYS_OK, CHP_SYS_NONFINITE);
     }
-  }
-  if (a.mode == ROW_LAST) {
-    for (int idx = tid; idx < C::TR * N; idx += C::THREADS) {
-      const int r = idx / N, j = idx % N;
-      const int row = i0 + r;
-      if (row < m) out[(long long)row * N + j] = (j < m) ? X[(size_t)(r + 1) * N + j + 1] : 0.0;
-    }
-    return;
-  }
-  // 3. R = inner rows of x;  X <- w = x^3 - 3x
-  for (int idx = tid; idx < C::TR * N; idx += C::THREADS) R[idx] = X[idx + N];
-  __syncthreads();
-  for (int idx = tid; idx < (C::TR + 2) * N; idx += C::THREADS) {
-    const double x = X[idx];
-    X[idx] = fma(x, x * x, -3.0 * x);
+    if (last) return;
   }
   __syncthreads();
-  // 4. rhs = x + dt * L w  (CSR order: (i-1,j), (i,j-1), (i,j), (i,j+1), (i+1,j))
+
+  // -- phase 2: inner tile rows (1+2g, 2+2g) -> Q --------------------------------
+  // (L w) (FIRST: x + dt L w) into registers, block barrier, then into this
+  // group's phase-1 rows, which become the transform's input and scratch.
+  const bool active = g < C::GPB - 1;
+  const int r0 = 1 + 2 * g;                       // tile row of the first inner row
+  const int qa = i0 + 2 * g, qb = qa + 1;         // their global rows
+  const bool oa = active && qa < m, ob = active && qb < m;
+  const bool first = a.mode == ROW_FIRST;
   const double c = a.c1, c4 = -4.0 * a.c1, dt = a.dt;
-  for (int idx = tid; idx < C::TR * N; idx += C::THREADS) {
-    const int r = idx / N, j = idx % N;
-    double v = 0.0;
-    if (j > 0) {
-      const double* w0 = X + (size_t)(r + 1) * N;
-      const double wl = w0[j - 1];                       // j-1 = 0 is the boundary (0)
-      const double wr = (j + 1 < N) ? w0[j + 1] : 0.0;
-      const double lw = (((X[(size_t)r * N + j] * c + wl * c) + w0[j] * c4) + wr * c) +
-                        X[(size_t)(r + 2) * N + j] * c;
-      v = R[idx] + dt * lw;
+  const double* qpa = in + (long long)(oa ? qa : 0) * N;
+  const double* qpb = in + (long long)(ob ? qb : 0) * N;
+  constexpr int PL = N / L;                       // values per lane per row
+  double la[PL], lb[PL];
+  auto lapw = [&](int r, int n) -> double {       // (L w) at tile row r, column n >= 1
+    const double* w0 = sm + (size_t)r * N;
+    const double wr = (n + 1 < N) ? w0[wdst::rsw(n + 1)] : 0.0;
+    return (((sm[(size_t)(r - 1) * N + wdst::rsw(n)] * c + w0[wdst::rsw(n - 1)] * c) +
+             w0[wdst::rsw(n)] * c4) + wr * c) + sm[(size_t)(r + 1) * N + wdst::rsw(n)] * c;
+  };
+#pragma unroll
+  for (int i = 0; i < PL; ++i) {
+    const int n = l + L * i;
+    double x = 0.0, y = 0.0;
+    if (active && n > 0) {
+      x = lapw(r0, n);
+      y = lapw(r0 + 1, n);
+      if (first) {   // Q = T_j(x + dt L w) from the physical input
+        x = (oa ? qpa[n] : 0.0) + dt * x;
+        y = (ob ? qpb[n] : 0.0) + dt * y;
+      }
     }
-    R[idx] = v;
+    la[i] = x;
+    lb[i] = y;
   }
   __syncthreads();
-  // 5. Q = T_j rhs
-  if (g < C::G - 1)
-    chpdst::dst_pair<N, C::T>(R + (size_t)g * 2 * N, tb, 1.0, ws + g * (C::T / 32), t, g + 1);
-  __syncthreads();
-  for (int idx = tid; idx < C::TR * N; idx += C::THREADS) {
-    const int r = idx / N, j = idx % N;
-    const int row = i0 + r;
-    if (row < m) out[(long long)row * N + j] = (j < m) ? R[(size_t)r * N + j + 1] : 0.0;
+#pragma unroll
+  for (int i = 0; i < PL; ++i) {
+    wr0[wdst::rsw(l + L * i)] = la[i];
+    wr1[wdst::rsw(l + L * i)] = lb[i];
   }
+  __syncwarp();
+  auto ld2 = [&](int n, double& x, double& xm, double& y, double& ym) {
+    const bool z0 = (n == 0);
+    x = z0 ? 0.0 : wr0[wdst::rsw(n)];
+    xm = z0 ? 0.0 : wr0[wdst::rsw(N - n)];
+    y = z0 ? 0.0 : wr1[wdst::rsw(n)];
+    ym = z0 ? 0.0 : wr1[wdst::rsw(N - n)];
+  };
+  const double half = 0.5 * N;
+  auto st2 = [&](int k, double a2, double a21, double b2, double b21) {
+    if (first) {
+      if (oa) *reinterpret_cast<double2*>(out + (long long)qa * N + 2 * k) = make_double2(a2, a21);
+      if (ob) *reinterpret_cast<double2*>(out + (long long)qb * N + 2 * k) = make_double2(b2, b21);
+      return;
+    }
+    if (oa) {
+      const double2 p = *reinterpret_cast<const double2*>(qpa + 2 * k);
+      *reinterpret_cast<double2*>(out + (long long)qa * N + 2 * k) =
+          make_double2(k == 0 ? 0.0 : fma(half, p.x, dt * a2), fma(half, p.y, dt * a21));
+    }
+    if (ob) {
+      const double2 p = *reinterpret_cast<const double2*>(qpb + 2 * k);
+      *reinterpret_cast<double2*>(out + (long long)qb * N + 2 * k) =
+          make_double2(k == 0 ? 0.0 : fma(half, p.x, dt * b2), fma(half, p.y, dt * b21));
+    }
+  };
+  wdst::pair_dst<N>(ld2, st2, scr, twt, l, ac);
 }
 
 // ---------------------------------------------------------------------------
-// Column pass: P = T_i (D' .* T_i Q), in place.
+// LINEAR_B column pass: P = T_i (D' .* T_i Q), in place
 // ---------------------------------------------------------------------------
 struct ColArgs {
   double* buf;
@@ -153,45 +221,76 @@ struct ColArgs {
   int m;
   double a2dt, b, scale;   // den = (1 - a2dt*lam) + b*lam^2 ; scale = (2/N)^2
   const double* lam;       // lam[p], p = 1..m (index 0 unused)
+  const double2* wtab;
 };
 
 template <int N>
-__global__ void __launch_bounds__(Cfg<N>::THREADS)
-k2d_col_pass_b(ColArgs a, Tables tb) {
-  using C = Cfg<N>;
-  extern __shared__ double sm[];
-  double* ws = sm + (size_t)C::TC * N;
+CHP_DEV int csw(int c, int n) { return c * N + (n ^ c ^ (((n >> 5) & 15) << 1)); }
+
+template <int N>
+__global__ void __launch_bounds__(WCfg<N>::THREADS)
+k2d_col_pass_b(ColArgs a) {
+  using C = WCfg<N>;
+  constexpr int L = C::L, TC = C::TC;
+  extern __shared__ __align__(16) double sm[];    // 2*GPB columns of N (swizzled) + twiddles
+  double2* twt = reinterpret_cast<double2*>(sm + (size_t)(2 * C::GPB) * N);
   const int tid = threadIdx.x;
-  const int g = tid / C::T, t = tid % C::T;
+  const int g = tid / L, l = tid % L;
   const int s = blockIdx.y;
   const int m = a.m;
-  const int j0 = blockIdx.x * C::TC;
+  const int j0 = blockIdx.x * TC;                 // storage column of tile column 0
   double* buf = a.buf + (long long)s * a.stride;
-  // load: column c -> sm[c*N + i + 1]
-  for (int idx = tid; idx < m * C::TC; idx += C::THREADS) {
-    const int i = idx / C::TC, c = idx % C::TC;
-    sm[(size_t)c * N + i + 1] = (j0 + c < m) ? buf[(long long)i * N + j0 + c] : 0.0;
+  wdst::load_twiddles<N>(twt, a.wtab + N);
+  const double2 ac = __ldg(&a.wtab[l]);
+  // logical (column c, math row n) at csw(c, n)
+  for (int idx = tid; idx < N * TC; idx += C::THREADS) {
+    const int n = idx / TC, cc = idx % TC;
+    sm[csw<N>(cc, n)] = (n > 0) ? buf[(long long)(n - 1) * N + j0 + cc] : 0.0;
   }
-  if (tid < C::TC) sm[(size_t)tid * N] = 0.0;
   __syncthreads();
-  double* pr = sm + (size_t)g * 2 * N;
-  chpdst::dst_pair<N, C::T>(pr, tb, 1.0, ws + g * (C::T / 32), t, g + 1);
-  // scale by D' (each group scales its own pair)
-  for (int idx = t; idx < 2 * N; idx += C::T) {
-    const int c = 2 * g + idx / N, p = idx % N;
-    const int q = j0 + c + 1;
-    if (p > 0 && q <= m) {
-      const double lam = a.lam[p] + a.lam[q];
-      const double den = (1.0 - a.a2dt * lam) + a.b * (lam * lam);
-      pr[idx] = pr[idx] * (a.scale / den);
+  // groups beyond the tile (small N) run on zeros so every lane of the warp
+  // takes part in pair_dst's shuffles / __syncwarp
+  const int ca = 2 * g, cb = ca + 1;
+  const bool grp = ca < TC;
+  double2* scr = reinterpret_cast<double2*>(sm + (size_t)ca * N);
+  const int qa = j0 + ca, qb = j0 + cb;           // math column indices
+  bool scale_pass = true;
+  auto ld = [&](int n, double& x, double& xm, double& y, double& ym) {
+    const bool z = !grp || n == 0;
+    x = z ? 0.0 : sm[csw<N>(ca, n)];
+    xm = z ? 0.0 : sm[csw<N>(ca, N - n)];
+    y = z ? 0.0 : sm[csw<N>(cb, n)];
+    ym = z ? 0.0 : sm[csw<N>(cb, N - n)];
+  };
+  auto dscale = [&](int p, int q) -> double {
+    if (p == 0 || q == 0) return 0.0;
+    const double lam = a.lam[p] + a.lam[q];
+    return a.scale * wdst::rcp((1.0 - a.a2dt * lam) + a.b * (lam * lam));
+  };
+  auto st = [&](int k, double a2, double a21, double b2, double b21) {
+    if (!grp) return;
+    if (scale_pass) {
+      a2 *= dscale(2 * k, qa);
+      a21 *= dscale(2 * k + 1, qa);
+      b2 *= dscale(2 * k, qb);
+      b21 *= dscale(2 * k + 1, qb);
     }
+    sm[csw<N>(ca, 2 * k)] = a2;
+    sm[csw<N>(ca, 2 * k + 1)] = a21;
+    sm[csw<N>(cb, 2 * k)] = b2;
+    sm[csw<N>(cb, 2 * k + 1)] = b21;
+  };
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    scale_pass = (pass == 0);
+    wdst::pair_dst<N>(ld, st, scr, twt, l, ac);
+    __syncwarp();
   }
-  chpdst::group_sync(g + 1, C::T);
-  chpdst::dst_pair<N, C::T>(pr, tb, 1.0, ws + g * (C::T / 32), t, g + 1);
   __syncthreads();
-  for (int idx = tid; idx < m * C::TC; idx += C::THREADS) {
-    const int i = idx / C::TC, c = idx % C::TC;
-    if (j0 + c < m) buf[(long long)i * N + j0 + c] = sm[(size_t)c * N + i + 1];
+  for (int idx = tid; idx < m * TC; idx += C::THREADS) {
+    const int i = idx / TC, cc = idx % TC;
+    const int j = j0 + cc;
+    buf[(long long)i * N + j] = (j > 0) ? sm[csw<N>(cc, i + 1)] : 0.0;
   }
 }
 
@@ -242,7 +341,7 @@ k2d_rowdst(RowDst a, Tables tb) {
   double* out = a.out + (long long)s * a.stride;
   for (int idx = tid; idx < TRg * N; idx += C::THREADS) {
     const int r = idx / N, j = idx % N, row = i0 + r;
-    sm[idx] = (j > 0 && row < m) ? in[(long long)row * N + j - 1] : 0.0;
+    sm[idx] = (j > 0 && row < m) ? in[(long long)row * N + j] : 0.0;
   }
   __syncthreads();
   chpdst::dst_pair<N, C::T>(sm + (size_t)g * 2 * N, tb, a.scale, ws + g * (C::T / 32), t, g + 1);
@@ -251,9 +350,9 @@ k2d_rowdst(RowDst a, Tables tb) {
   for (int idx = tid; idx < TRg * N; idx += C::THREADS) {
     const int r = idx / N, j = idx % N, row = i0 + r;
     if (row >= m) continue;
-    double v = (j < m) ? sm[(size_t)r * N + j + 1] : 0.0;
-    if (a.op == 1 && j < m) {
-      const double kap = -(a.lam[row + 1] + a.lam[j + 1]);
+    double v = (j > 0) ? sm[(size_t)r * N + j] : 0.0;
+    if (a.op == 1 && j > 0) {
+      const double kap = -(a.lam[row + 1] + a.lam[j]);
       const double d = 1.0 / kap + a.b * kap;
       const double pv = a.p[(long long)s * a.stride + (long long)row * N + j];
       v = fma(d, pv, v);
@@ -300,7 +399,7 @@ k2d_coldst(ColDst a, Tables tb) {
   double* out = a.out + (long long)s * a.stride;
   for (int idx = tid; idx < m * C::TC; idx += C::THREADS) {
     const int i = idx / C::TC, c = idx % C::TC;
-    sm[(size_t)c * N + i + 1] = (j0 + c < m) ? in[(long long)i * N + j0 + c] : 0.0;
+    sm[(size_t)c * N + i + 1] = (j0 + c > 0) ? in[(long long)i * N + j0 + c] : 0.0;
   }
   if (tid < C::TC) sm[(size_t)tid * N] = 0.0;
   __syncthreads();
@@ -310,20 +409,20 @@ k2d_coldst(ColDst a, Tables tb) {
     const double* cs = a.c + (long long)s * a.stride;
     for (int idx = t; idx < 2 * N; idx += C::T) {
       const int c = 2 * g + idx / N, p = idx % N, q = j0 + c;
-      if (p > 0 && q < m) pr[idx] *= a.scale * cs[(long long)(p - 1) * N + q];
+      if (p > 0 && q > 0) pr[idx] *= a.scale * cs[(long long)(p - 1) * N + q];
     }
     chpdst::group_sync(g + 1, C::T);
     chpdst::dst_pair<N, C::T>(pr, tb, 1.0, ws + g * (C::T / 32), t, g + 1);
   } else if (a.op == 2) {
     for (int idx = t; idx < 2 * N; idx += C::T) {
-      const int c = 2 * g + idx / N, p = idx % N, q = j0 + c + 1;
-      if (p > 0 && q <= m) pr[idx] *= a.scale / (-(a.lam[p] + a.lam[q]));
+      const int c = 2 * g + idx / N, p = idx % N, q = j0 + c;
+      if (p > 0 && q > 0) pr[idx] *= a.scale / (-(a.lam[p] + a.lam[q]));
     }
   }
   __syncthreads();
   for (int idx = tid; idx < m * C::TC; idx += C::THREADS) {
     const int i = idx / C::TC, c = idx % C::TC;
-    if (j0 + c < m) out[(long long)i * N + j0 + c] = sm[(size_t)c * N + i + 1];
+    out[(long long)i * N + j0 + c] = (j0 + c > 0) ? sm[(size_t)c * N + i + 1] : 0.0;
   }
 }
 
@@ -334,7 +433,7 @@ CHP_DEV void for_points(int m, int N, F f) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(t / m), j = (int)(t % m);
-    f(i, j, (long long)i * N + j);
+    f(i, j, (long long)i * N + j + 1);
   }
 }
 
@@ -350,13 +449,13 @@ CHP_DEV double block_sum(double v, double* ws) {
 }
 
 CHP_DEV double at(const double* f, int i, int j, int m, int N) {
-  return (i >= 0 && i < m && j >= 0 && j < m) ? f[(long long)i * N + j] : 0.0;
+  return (i >= 0 && i < m && j >= 0 && j < m) ? f[(long long)i * N + j + 1] : 0.0;
 }
 
 // 5-point L in the CSR order of grid.py:110 (rows (i-1,j),(i,j-1),(i,j),(i,j+1),(i+1,j))
 CHP_DEV double lap5(const double* f, int i, int j, int m, int N, double c) {
   return ((((at(f, i - 1, j, m, N) * c + at(f, i, j - 1, m, N) * c) +
-            f[(long long)i * N + j] * (-4.0 * c)) + at(f, i, j + 1, m, N) * c) +
+            f[(long long)i * N + j + 1] * (-4.0 * c)) + at(f, i, j + 1, m, N) * c) +
           at(f, i + 1, j, m, N) * c);
 }
 
@@ -592,7 +691,7 @@ __global__ void k2d_scatter(Pt pt, const double* x, double* dst, long long dst_s
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)pt.m * pt.N;
        t += (long long)gridDim.x * blockDim.x) {
     const int j = (int)(t % pt.N);
-    const double v = (j < pt.m) ? xs[t] : 0.0;
+    const double v = (j > 0) ? xs[t] : 0.0;
     d[t] = v;
     bad |= !isfinite(v);
   }
@@ -671,6 +770,7 @@ struct NTables {
   double2* tw = nullptr;
   double* sj = nullptr;
   double* lam = nullptr;   // per-axis eigenvalues, index p = 1..m
+  double2* wtab = nullptr; // wdst lane tables: (cos, sin)(pi l/N), then W_N^l
 };
 
 struct Work2 {            // device workspace for one solve batch
@@ -687,9 +787,9 @@ void set_smem_attrs() {
   static bool done = false;
   if (done) return;
   cudaFuncSetAttribute(k2d_row_pass<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)Cfg<N>::ROW_SMEM);
+                       (int)WCfg<N>::ROW_SMEM);
   cudaFuncSetAttribute(k2d_col_pass_b<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)Cfg<N>::COL_SMEM);
+                       (int)WCfg<N>::COL_SMEM);
   cudaFuncSetAttribute(k2d_rowdst<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(double) * (2 * Cfg<N>::G * N + Cfg<N>::G * (Cfg<N>::T / 32))));
   cudaFuncSetAttribute(k2d_coldst<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -702,32 +802,33 @@ cudaError_t run_linear_b(const chp_grid& g, const chp_spec& sp, int steps, int n
                          const double* in, long long in_stride, double* out, long long out_stride,
                          const int* sys_index, chp_sys_info* info, const NTables& nt,
                          double* scratch, cudaStream_t st) {
-  using C = Cfg<N>;
+  using C = WCfg<N>;
   set_smem_attrs<N>();
-  const Tables tb{nt.tw, nt.sj};
   const int m = g.m;
   const long long fs = (long long)m * N;
   double* buf[2] = {scratch, scratch + fs * nsys};
-  const dim3 rgrid((m + C::TR - 1) / C::TR, nsys), cgrid((m + C::TC - 1) / C::TC, nsys);
-  ColArgs ca{nullptr, fs, m, 2.0 * sp.dt, sp.b, (2.0 / N) * (2.0 / N), nt.lam};
+  const dim3 rgrid((m + C::TR - 1) / C::TR, nsys), cgrid(N / C::TC, nsys);
+  ColArgs ca{nullptr, fs, m, 2.0 * sp.dt, sp.b, (2.0 / N) * (2.0 / N), nt.lam, nt.wtab};
   for (int s = 0; s < steps; ++s) {
     RowArgs ra{};
     ra.m = m; ra.dt = sp.dt; ra.c1 = g.c1; ra.info = info; ra.info_index = sys_index;
+    ra.wtab = nt.wtab;
     if (s == 0) {
       ra.in = in; ra.in_stride = in_stride; ra.in_index = sys_index; ra.mode = ROW_FIRST;
     } else {
       ra.in = buf[(s - 1) & 1]; ra.in_stride = fs; ra.in_index = nullptr; ra.mode = ROW_MID;
     }
     ra.out = buf[s & 1]; ra.out_stride = fs; ra.out_index = nullptr;
-    k2d_row_pass<N><<<rgrid, C::THREADS, C::ROW_SMEM, st>>>(ra, tb);
+    k2d_row_pass<N><<<rgrid, C::THREADS, C::ROW_SMEM, st>>>(ra);
     ca.buf = buf[s & 1];
-    k2d_col_pass_b<N><<<cgrid, C::THREADS, C::COL_SMEM, st>>>(ca, tb);
+    k2d_col_pass_b<N><<<cgrid, C::THREADS, C::COL_SMEM, st>>>(ca);
   }
   RowArgs ra{};
   ra.m = m; ra.dt = sp.dt; ra.c1 = g.c1; ra.info = info; ra.info_index = sys_index;
+  ra.wtab = nt.wtab;
   ra.in = buf[(steps - 1) & 1]; ra.in_stride = fs; ra.in_index = nullptr; ra.mode = ROW_LAST;
   ra.out = out; ra.out_stride = out_stride; ra.out_index = sys_index;
-  k2d_row_pass<N><<<rgrid, C::THREADS, C::ROW_SMEM, st>>>(ra, tb);
+  k2d_row_pass<N><<<rgrid, C::THREADS, C::ROW_SMEM, st>>>(ra);
   return cudaGetLastError();
 }
 
@@ -744,7 +845,7 @@ cudaError_t pcg_solve(const chp_grid& g, int nsys, double a, double b, double to
   const int m = g.m;
   const long long fs = (long long)m * N;
   const int rtiles = (m + 2 * C::G - 1) / (2 * C::G);
-  const dim3 rgrid(rtiles, nsys), cgrid((m + C::TC - 1) / C::TC, nsys), egrid(kPB, nsys);
+  const dim3 rgrid(rtiles, nsys), cgrid(N / C::TC, nsys), egrid(kPB, nsys);
   const size_t rsm = sizeof(double) * (2 * C::G * N + C::G * (C::T / 32));
   const Pt pt{m, N, fs, g.c1, nullptr, nullptr};
   const int red_blocks = (nsys + 7) / 8;
@@ -838,6 +939,7 @@ void chp2d_destroy(Chp2d* c) {
     cudaFree(kv.second.tw);
     cudaFree(kv.second.sj);
     cudaFree(kv.second.lam);
+    cudaFree(kv.second.wtab);
   }
   if (c->scratch) cudaFree(c->scratch);
   if (c->work) cudaFree(c->work);
@@ -866,8 +968,21 @@ cudaError_t get_tables(Chp2d* c, int N, const NTables** out) {
     const long double sp = sinl(pi * p / (2.0L * N));
     lam[p] = (double)(-4.0L / (h * h) * sp * sp);
   }
+  std::vector<double2> wt(2 * N);
+  int wl = 2;                                  // lanes of the wdst geometry for N
+  while (wl * wl * 2 <= N && wl < 32) wl *= 2;  // 8->2 16->4 32->4 64->8 ... 1024->32
+  if (wl * wl > N) wl /= 2;
+  for (int l = 0; l < N; ++l)
+    wt[l] = make_double2((double)cosl(pi * l / N), (double)sinl(pi * l / N));
+  for (int k2 = 0; k2 < N / wl; ++k2)
+    for (int l = 0; l < wl; ++l) {
+      const long double ang = 2.0L * pi * (long double)((l * k2) % N) / N;
+      wt[N + k2 * wl + l] = make_double2((double)cosl(ang), (double)-sinl(ang));
+    }
   NTables t;
   cudaError_t e;
+  if ((e = cudaMalloc(&t.wtab, sizeof(double2) * 2 * N)) != cudaSuccess) return e;
+  cudaMemcpy(t.wtab, wt.data(), sizeof(double2) * 2 * N, cudaMemcpyHostToDevice);
   if ((e = cudaMalloc(&t.tw, sizeof(double2) * N)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.sj, sizeof(double) * (N + 1))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.lam, sizeof(double) * N)) != cudaSuccess) return e;

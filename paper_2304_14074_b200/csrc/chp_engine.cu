@@ -15,7 +15,8 @@ __global__ void k_max_abs_diff(int rows, int m, int pitch, int n, const double* 
     const long long f = t / per;
     const long long r = (t % per) / m;
     const long long j = t % m;
-    const double d = fabs(a[f * as + r * pitch + j] - b[f * bs + r * pitch + j]);
+    const long long o = r * pitch + (pitch - m) + j;   // 2D rows lead with the pad
+    const double d = fabs(a[f * as + o] - b[f * bs + o]);
     mx = (d > mx || d != d) ? d : mx;
   }
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));

@@ -59,8 +59,9 @@ class SpatialGrid:
 
     @property
     def pitch(self) -> int:
-        """Device row pitch: 2D rows are padded to m+1 doubles (16-byte aligned,
-        one zero Dirichlet ghost per row); 1D fields are unpadded."""
+        """Device row pitch: a 2D row is [0, v_1 .. v_m] (m+1 = N doubles: the
+        leading zero is the Dirichlet boundary, so storage index = math index and
+        rows are 16-byte aligned); 1D fields are unpadded."""
         m = self.interior_per_axis
         return m if self.dim == 1 else m + 1
 
@@ -167,7 +168,8 @@ def to_device_layout(grid: SpatialGrid, flat, device=None, out=None):
         return t.contiguous()
     dst = out if out is not None else torch.zeros((m, grid.pitch), dtype=torch.float64,
                                                   device=device)
-    dst[:, :m].copy_(flat.view(m, m), non_blocking=True)
+    dst[:, 0] = 0.0                                   # leading Dirichlet pad column
+    dst[:, 1:].copy_(flat.view(m, m), non_blocking=True)
     return dst
 
 
@@ -176,7 +178,7 @@ def from_device_layout(grid: SpatialGrid, dev):
     if grid.dim == 1:
         return dev.reshape(-1)
     m = grid.interior_per_axis
-    return dev.reshape(m, grid.pitch)[:, :m].reshape(-1)
+    return dev.reshape(m, grid.pitch)[:, 1:].reshape(-1)
 
 
 class DiscreteOperator:

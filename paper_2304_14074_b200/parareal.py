@@ -280,8 +280,8 @@ def _record(eng: PararealEngine, R, eps: float, wall: float, inc=None) -> Iterat
     m = g.interior_per_axis
     U = eng.U[0]
     if g.dim == 2:
-        Uv = U.view(eng.N + 1, m, g.pitch)[:, :, :m]
-        diff = (Uv - R[0].view(eng.N + 1, m, g.pitch)[:, :, :m]) if R is not None else None
+        Uv = U.view(eng.N + 1, m, g.pitch)[:, :, 1:]
+        diff = (Uv - R[0].view(eng.N + 1, m, g.pitch)[:, :, 1:]) if R is not None else None
     else:
         Uv = U
         diff = (U - R[0]) if R is not None else None
