@@ -100,7 +100,7 @@ def count_launches(fn):
     for ev in prof.events():
         nm = ev.name
         if any(s in nm for s in ("k2d_", "k1d_", "k_max_abs_diff")):
-            short = nm.split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+            short = nm.replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "").split("(")[0]
             names[short] = names.get(short, 0) + 1
     return sum(names.values()), names
 

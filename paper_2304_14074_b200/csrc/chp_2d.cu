@@ -18,6 +18,7 @@
 //                P = T_i (D' .* T_i Q),  D' = (2/N)^2 D
 // J steps = J+1 row passes + J column passes, every slice of every IC in
 // each launch.
+#include <cooperative_groups.h>
 #include <math.h>
 
 #include <map>
@@ -54,6 +55,16 @@ template <int N> struct WCfg {
   static constexpr int TR = ROWS - 2;              // inner rows per row tile
   static constexpr int TC = (2 * GPB < N) ? 2 * GPB : N;   // columns per column tile
   static constexpr size_t ROW_SMEM = sizeof(double) * (size_t)ROWS * N + 16 * (size_t)N;
+  static constexpr size_t COL_SMEM = sizeof(double) * (size_t)(2 * GPB) * N + 16 * (size_t)N;
+};
+
+// column pass: smaller blocks (no halo), so that two blocks overlap on an SM
+template <int N> struct WCfgC {
+  static constexpr int L = wdst::Geo<N>::L;
+  static constexpr int WARPS = (N >= 64) ? 4 : 1;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int GPB = THREADS / L;
+  static constexpr int TC = (2 * GPB < N) ? 2 * GPB : N;
   static constexpr size_t COL_SMEM = sizeof(double) * (size_t)(2 * GPB) * N + 16 * (size_t)N;
 };
 
@@ -228,9 +239,9 @@ template <int N>
 CHP_DEV int csw(int c, int n) { return c * N + (n ^ c ^ (((n >> 5) & 15) << 1)); }
 
 template <int N>
-__global__ void __launch_bounds__(WCfg<N>::THREADS)
+__global__ void __launch_bounds__(WCfgC<N>::THREADS, 2)
 k2d_col_pass_b(ColArgs a) {
-  using C = WCfg<N>;
+  using C = WCfgC<N>;
   constexpr int L = C::L, TC = C::TC;
   extern __shared__ __align__(16) double sm[];    // 2*GPB columns of N (swizzled) + twiddles
   double2* twt = reinterpret_cast<double2*>(sm + (size_t)(2 * C::GPB) * N);
@@ -243,6 +254,7 @@ k2d_col_pass_b(ColArgs a) {
   wdst::load_twiddles<N>(twt, a.wtab + N);
   const double2 ac = __ldg(&a.wtab[l]);
   // logical (column c, math row n) at csw(c, n)
+#pragma unroll 8
   for (int idx = tid; idx < N * TC; idx += C::THREADS) {
     const int n = idx / TC, cc = idx % TC;
     sm[csw<N>(cc, n)] = (n > 0) ? buf[(long long)(n - 1) * N + j0 + cc] : 0.0;
@@ -287,6 +299,7 @@ k2d_col_pass_b(ColArgs a) {
     __syncwarp();
   }
   __syncthreads();
+#pragma unroll 8
   for (int idx = tid; idx < m * TC; idx += C::THREADS) {
     const int i = idx / TC, cc = idx % TC;
     const int j = j0 + cc;
@@ -764,6 +777,427 @@ __global__ void k2d_newton_norm(int nsys, const double* partial, double hd, doub
 }
 
 // ---------------------------------------------------------------------------
+// Device-resident coarse sweep (LINEAR_A coarse propagator, 2D): ONE
+// cooperative persistent kernel runs the whole sequential recursion
+//   for n in [n0, n1):  g = G(U_n) by DST-preconditioned CG;
+//                       U_{n+1} = (g + F_n) - G_n;  G_n = g      (parareal.py:245-251)
+// with grid-wide barriers between phases and no host round trip.  Every
+// reduction is block partials -> a fixed-order sum that every block
+// recomputes identically, so all blocks take the same branches and the
+// result is bitwise reproducible.
+// ---------------------------------------------------------------------------
+struct CoopArgs {
+  int m, nic, nsl, n0, n1, mode;
+  double c1, dt, b, tol;
+  int max_iter, pad_;
+  double* U; const double* F; double* G; long long ics, sls;
+  unsigned char* changed; double* inc; chp_sys_info* info;
+  double *X, *Rv, *Pv, *Yv, *Cv, *CT;   // per-IC work fields (stride fs), nic-major
+  double* part;                          // [2][gridDim][8] block partials
+  unsigned int* bar;                     // grid barrier counter (zeroed by the host)
+  const double* lam; const double2* wtab;
+};
+
+// Grid-wide barrier for the co-resident (cooperative) launch: one relaxed
+// spin per block and one fence on each side, instead of a fence per poll.
+struct GridBar {
+  unsigned int* cnt;
+  unsigned int gen;
+};
+CHP_DEV void gbar(GridBar& b) {
+  __syncthreads();
+  b.gen += 1;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(b.cnt, 1u);
+    const unsigned int target = b.gen * gridDim.x;
+    unsigned int v;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(b.cnt) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int N>
+struct CoopCtx {
+  const CoopArgs& a;
+  double* sm;          // dynamic smem: GPB groups x 2N doubles, then twiddles (N double2)
+  double2* twt;
+  double* red;         // 32 doubles of static smem for block reductions
+  int tid, g, l, gpb, ngroups, gg;
+  double2 ac;
+  CHP_DEV long long fs() const { return (long long)a.m * N; }
+};
+
+// fixed-order block reduction of (v0..v3) into part[blockIdx][0..3]
+template <int K>
+CHP_DEV void coop_block_partials(double (&v)[K], double* red, double* part) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = v[k];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) * K + k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w * K + threadIdx.x];
+    part[blockIdx.x * 8 + threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
+// every block: fixed-order sum over all blocks' partials -> out[0..K)
+template <int K>
+CHP_DEV void coop_total(const double* part, double* red, double (&out)[K]) {
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double x = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) x += part[b * 8 + k];
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (threadIdx.x == 0) red[k] = x;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = red[k];
+  __syncthreads();
+}
+
+// row-pair DST over the field: dst rows = T_j src rows (+ optional CG op)
+//   op 0: dst = T_j src
+//   op 1: dst = d .* p + T_j src ; returns thread partial of p.q
+template <int N>
+__device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, double* dst, int op, const double* p) {
+  const auto& a = x.a;
+  const int m = a.m;
+  double part = 0.0;
+  double2* scr = reinterpret_cast<double2*>(x.sm + (size_t)x.g * 2 * N);
+  // whole warps iterate together (pair_dst needs every lane of the warp);
+  // groups without a pair run on zeros and store nothing
+  for (int it = 0;; ++it) {
+    const int pr = x.gg + it * x.ngroups;
+    const bool have = pr < (m + 1) / 2;
+    if (!__any_sync(0xffffffffu, have)) break;
+    const int ra = have ? 2 * pr : 0, rb = ra + 1;
+    const bool vb = have && rb < m;
+    const double* sa = src + (long long)ra * N;
+    const double* sb = src + (long long)(vb ? rb : ra) * N;
+    auto ld = [&](int n, double& u, double& um, double& v, double& vm) {
+      const bool z = n == 0 || !have;
+      u = z ? 0.0 : sa[n];
+      um = z ? 0.0 : sa[N - n];
+      v = (z || !vb) ? 0.0 : sb[n];
+      vm = (z || !vb) ? 0.0 : sb[N - n];
+    };
+    auto st = [&](int k, double a2, double a21, double b2, double b21) {
+      if (!have) return;
+      if (op == 1) {
+        const int r0 = ra;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + h;
+          if (r >= m) break;
+          double y0 = h ? b2 : a2, y1 = h ? b21 : a21;
+          const double2 pv = *reinterpret_cast<const double2*>(p + (long long)r * N + 2 * k);
+          const double k0 = -(a.lam[r + 1] + a.lam[2 * k]), k1 = -(a.lam[r + 1] + a.lam[2 * k + 1]);
+          if (k > 0) { y0 = fma(1.0 / k0 + a.b * k0, pv.x, y0); part = fma(pv.x, y0, part); }
+          else y0 = 0.0;
+          y1 = fma(1.0 / k1 + a.b * k1, pv.y, y1);
+          part = fma(pv.y, y1, part);
+          *reinterpret_cast<double2*>(dst + (long long)r * N + 2 * k) = make_double2(y0, y1);
+        }
+      } else {
+        *reinterpret_cast<double2*>(dst + (long long)ra * N + 2 * k) = make_double2(a2, a21);
+        if (vb) *reinterpret_cast<double2*>(dst + (long long)rb * N + 2 * k) = make_double2(b2, b21);
+      }
+    };
+    wdst::pair_dst<N>(ld, st, scr, x.twt, x.l, x.ac);
+    __syncwarp();
+  }
+  return part;
+}
+
+// column-pair DST over the field (in place allowed):
+//   op 0: dst = scale * T_i src
+//   op 1: dst = T_i ((scale * c) .* T_i src)
+//   op 2: dst = T_i src .* (scale / kappa)
+template <int N>
+__device__ __noinline__ void coop_cols(CoopCtx<N>& x, const double* src, double* dst, int op, double scale,
+                       const double* cT) {
+  // Block-tiled column pass: TC = 2*gpb columns per tile, coalesced tile
+  // load/store through shared memory (swizzle csw), one lane group per pair.
+  //   op 0: dst = scale * T_i src
+  //   op 1: dst = T_i ((scale * c) .* T_i src)   (cT: c transposed, [q][n])
+  //   op 2: dst = T_i src .* (scale / kappa)
+  const auto& a = x.a;
+  const int m = a.m;
+  const int TC = (8 < N) ? 8 : N;            // small tiles: spread over all SMs
+  const int ca = 2 * x.g, cb = ca + 1;
+  double2* scr = reinterpret_cast<double2*>(x.sm + (size_t)ca * N);
+  for (int tile = blockIdx.x; tile < N / TC; tile += gridDim.x) {
+    const int j0 = tile * TC;
+#pragma unroll 8
+    for (int idx = threadIdx.x; idx < N * TC; idx += blockDim.x) {
+      const int n = idx / TC, cc = idx % TC;
+      x.sm[csw<N>(cc, n)] = (n > 0 && j0 + cc > 0) ? src[(long long)(n - 1) * N + j0 + cc] : 0.0;
+    }
+    __syncthreads();
+    const int qa = j0 + ca, qb = j0 + cb;
+    const bool act = ca < TC;
+    auto ld = [&](int n, double& u, double& um, double& v, double& vm) {
+      const bool z = n == 0 || !act;
+      u = z ? 0.0 : x.sm[csw<N>(ca, n)];
+      um = z ? 0.0 : x.sm[csw<N>(ca, N - n)];
+      v = z ? 0.0 : x.sm[csw<N>(cb, n)];
+      vm = z ? 0.0 : x.sm[csw<N>(cb, N - n)];
+    };
+    int pass = 0;
+    auto st = [&](int k, double a2, double a21, double b2, double b21) {
+      if (!act) return;
+      const int p0 = 2 * k, p1 = p0 + 1;
+      if (op == 1 && pass == 0) {
+        const double2 c_a = *reinterpret_cast<const double2*>(cT + (long long)qa * N + p0);
+        const double2 c_b = *reinterpret_cast<const double2*>(cT + (long long)qb * N + p0);
+        a2 *= scale * c_a.x; a21 *= scale * c_a.y;
+        b2 *= scale * c_b.x; b21 *= scale * c_b.y;
+      } else if (op == 0) {
+        a2 *= scale; a21 *= scale; b2 *= scale; b21 *= scale;
+      } else if (op == 2) {
+        a2 = (p0 > 0 && qa > 0) ? a2 * (scale / (-(a.lam[p0] + a.lam[qa]))) : 0.0;
+        b2 = (p0 > 0) ? b2 * (scale / (-(a.lam[p0] + a.lam[qb]))) : 0.0;
+        a21 = (qa > 0) ? a21 * (scale / (-(a.lam[p1] + a.lam[qa]))) : 0.0;
+        b21 = b21 * (scale / (-(a.lam[p1] + a.lam[qb])));
+      }
+      x.sm[csw<N>(ca, p0)] = (qa > 0 && p0 > 0) ? a2 : 0.0;
+      x.sm[csw<N>(ca, p1)] = (qa > 0) ? a21 : 0.0;
+      x.sm[csw<N>(cb, p0)] = (p0 > 0) ? b2 : 0.0;
+      x.sm[csw<N>(cb, p1)] = b21;
+    };
+    // every group runs (small N: several groups share a warp); groups beyond
+    // the tile read zeros and store nothing
+    wdst::pair_dst<N>(ld, st, scr, x.twt, x.l, x.ac);
+    __syncwarp();
+    if (op == 1) {
+      pass = 1;
+      wdst::pair_dst<N>(ld, st, scr, x.twt, x.l, x.ac);
+      __syncwarp();
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int idx = threadIdx.x; idx < m * TC; idx += blockDim.x) {
+      const int i = idx / TC, cc = idx % TC;
+      const int j = j0 + cc;
+      dst[(long long)i * N + j] = (j > 0) ? x.sm[csw<N>(cc, i + 1)] : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
+  GridBar grid{a.bar, 0u};
+  extern __shared__ __align__(16) double smc[];
+  __shared__ double red[64];
+  constexpr int L = wdst::Geo<N>::L;
+  CoopCtx<N> x{a};
+  x.sm = smc;
+  x.gpb = blockDim.x / L;
+  x.twt = reinterpret_cast<double2*>(smc + (size_t)x.gpb * 2 * N);
+  x.red = red;
+  x.tid = threadIdx.x;
+  x.g = x.tid / L;
+  x.l = x.tid % L;
+  x.ngroups = gridDim.x * x.gpb;
+  x.gg = x.g * gridDim.x + blockIdx.x;       // spread pairs over all SMs first
+  x.ac = __ldg(&a.wtab[x.l]);
+  wdst::load_twiddles<N>(x.twt, a.wtab + N);
+  __syncthreads();
+  const int m = a.m;
+  const long long fs = (long long)m * N;
+  const long long tot = fs;
+  const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gstride = (long long)gridDim.x * blockDim.x;
+  const double s2 = (2.0 / N) * (2.0 / N);
+  const double tol2 = a.tol * a.tol;
+  int pb = 0;                                      // alternating partial buffer
+
+  for (int ic = 0; ic < a.nic; ++ic) {
+    double* X = a.X + ic * fs;
+    double* Rv = a.Rv + ic * fs;
+    double* Pv = a.Pv + ic * fs;
+    double* Yv = a.Yv + ic * fs;
+    double* Cv = a.Cv + ic * fs;
+    double* CT = a.CT + ic * fs;
+    unsigned char* ch = a.changed ? a.changed + (long long)ic * (a.nsl + 1) : nullptr;
+    double* Ui = a.U + ic * a.ics;
+    double* Gi = a.G + ic * a.ics;
+    const double* Fi = a.F ? a.F + ic * a.ics : nullptr;
+    if (a.mode == 1 && (ch[0] & 2)) continue;    // IC frozen
+    double dmax = 0.0;
+    for (int n = a.n0; n < a.n1; ++n) {
+      const double* un = Ui + (long long)n * a.sls;
+      double* un1 = Ui + (long long)(n + 1) * a.sls;
+      double* gn = Gi + (long long)n * a.sls;
+      if (a.mode == 1 && blockIdx.x == 0 && threadIdx.x == 0) ch[n + 1] = 0;
+      gbar(grid);                                   // ch[n] / U_n written by the previous slice
+      const bool solve = (a.mode == 0) || (*(volatile unsigned char*)&ch[n] & 1);
+      if (solve) {
+        // ---- prep: rhs = v - dt L v (into Yv), c = v^2, sum c ------------------
+        double sc[1] = {0.0};
+        for (long long t = gtid; t < tot; t += gstride) {
+          const int i = (int)(t / N), j = (int)(t % N);
+          double r = 0.0, cv = 0.0;
+          if (j > 0) {
+            const double v = un[t];
+            const double vu = i > 0 ? un[t - N] : 0.0, vd = i + 1 < m ? un[t + N] : 0.0;
+            const double vl = j > 1 ? un[t - 1] : 0.0, vr = j < m ? un[t + 1] : 0.0;
+            const double lv = ((((vu * a.c1 + vl * a.c1) + v * (-4.0 * a.c1)) + vr * a.c1) + vd * a.c1);
+            r = v - a.dt * lv;
+            cv = v * v;
+          }
+          Yv[t] = r;
+          Cv[t] = cv;
+          sc[0] += cv;
+        }
+        double* pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
+        coop_block_partials<1>(sc, red, pbuf);
+        gbar(grid);
+        double tc[1];
+        coop_total<1>(pbuf, red, tc);
+        const double acbar = a.dt * (tc[0] / ((double)m * m));
+        // c transposed for the column phases: CT[q][n] = c[n-1][q]
+        for (long long t = gtid; t < tot; t += gstride) {
+          const int q = (int)(t / N), nn = (int)(t % N);
+          CT[t] = (nn > 0 && q > 0) ? Cv[(long long)(nn - 1) * N + q] : 0.0;
+        }
+        // ---- b^ = (2/N)/kappa .* T_i T_j rhs -> Rv -----------------------------
+        coop_rows<N>(x, Yv, Yv, 0, nullptr);
+        gbar(grid);
+        coop_cols<N>(x, Yv, Rv, 2, 2.0 / N, nullptr);
+        gbar(grid);
+        // ---- x = 0, p = r / M, rho = r.z, rr0 = r.r ---------------------------
+        double pr[2] = {0.0, 0.0};
+        for (long long t = gtid; t < tot; t += gstride) {
+          const int i = (int)(t / N), j = (int)(t % N);
+          X[t] = 0.0;
+          double z = 0.0;
+          if (j > 0) {
+            const double kap = -(a.lam[i + 1] + a.lam[j]);
+            const double M = (1.0 / kap + a.b * kap) + acbar;
+            const double rv = Rv[t];
+            z = rv / M;
+            pr[0] = fma(rv, z, pr[0]);
+            pr[1] = fma(rv, rv, pr[1]);
+          }
+          Pv[t] = z;
+        }
+        pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
+        coop_block_partials<2>(pr, red, pbuf);
+        gbar(grid);
+        double t0[2];
+        coop_total<2>(pbuf, red, t0);
+        double rho = t0[0];
+        const double rr0 = t0[1];
+        int it = 0;
+        bool fail = false;
+        bool done = !(rr0 > 0.0);
+        while (!done) {
+          coop_rows<N>(x, Pv, Yv, 0, nullptr);
+          gbar(grid);
+          coop_cols<N>(x, Yv, Yv, 1, a.dt * s2, CT);
+          gbar(grid);
+          double pq[1];
+          pq[0] = coop_rows<N>(x, Yv, Yv, 1, Pv);
+          pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
+          coop_block_partials<1>(pq, red, pbuf);
+          gbar(grid);
+          double tq[1];
+          coop_total<1>(pbuf, red, tq);
+          const double alpha = rho / tq[0];
+          double rz[2] = {0.0, 0.0};
+          for (long long t = gtid; t < tot; t += gstride) {
+            const int i = (int)(t / N), j = (int)(t % N);
+            if (j == 0) continue;
+            X[t] = fma(alpha, Pv[t], X[t]);
+            const double rv = fma(-alpha, Yv[t], Rv[t]);
+            Rv[t] = rv;
+            const double kap = -(a.lam[i + 1] + a.lam[j]);
+            const double M = (1.0 / kap + a.b * kap) + acbar;
+            rz[0] = fma(rv, rv / M, rz[0]);
+            rz[1] = fma(rv, rv, rz[1]);
+          }
+          pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
+          coop_block_partials<2>(rz, red, pbuf);
+          gbar(grid);
+          double t1[2];
+          coop_total<2>(pbuf, red, t1);
+          const double beta = t1[0] / rho;
+          rho = t1[0];
+          ++it;
+          if (!(t1[1] > tol2 * rr0)) done = true;
+          else if (it >= a.max_iter) { done = true; fail = true; }
+          if (!isfinite(t1[1])) { done = true; fail = true; }
+          if (done) break;
+          for (long long t = gtid; t < tot; t += gstride) {
+            const int i = (int)(t / N), j = (int)(t % N);
+            if (j == 0) continue;
+            const double kap = -(a.lam[i + 1] + a.lam[j]);
+            const double M = (1.0 / kap + a.b * kap) + acbar;
+            Pv[t] = fma(beta, Pv[t], Rv[t] / M);
+          }
+          gbar(grid);
+        }
+        if (gtid == 0) {
+          a.info[ic].cg_total += it;
+          a.info[ic].cg_max = max(a.info[ic].cg_max, it);
+          if (fail) atomicCAS(&a.info[ic].status, CHP_SYS_OK, CHP_SYS_CG);
+        }
+        // ---- g = (2/N) T_i T_j x -> Yv ---------------------------------------
+        coop_rows<N>(x, X, Yv, 0, nullptr);
+        gbar(grid);
+        coop_cols<N>(x, Yv, Yv, 0, 2.0 / N, nullptr);
+        gbar(grid);
+      }
+      // ---- correction / init ---------------------------------------------------
+      const double* gsrc = solve ? Yv : gn;
+      bool any = false, bad = false;
+      for (long long t = gtid; t < tot; t += gstride) {
+        const int j = (int)(t % N);
+        const double gv = (j > 0) ? gsrc[t] : 0.0;
+        if (a.mode == 0) {
+          un1[t] = gv;
+          gn[t] = gv;
+          bad |= !isfinite(gv);
+          continue;
+        }
+        const double nv = (gv + Fi[(long long)n * a.sls + t]) - gn[t];
+        const double ov = un1[t];
+        any |= (__double_as_longlong(nv) != __double_as_longlong(ov));
+        dmax = fmax(dmax, fabs(nv - ov));
+        bad |= !isfinite(nv) || !isfinite(gv);
+        un1[t] = nv;
+        gn[t] = gv;
+      }
+      if (a.mode == 1) {
+        // changed[n+1]: any block saw a differing bit (zeroed by the host first)
+        if (__syncthreads_or(any) && threadIdx.x == 0) ch[n + 1] = 1;
+      }
+      if (__syncthreads_or(bad) && threadIdx.x == 0)
+        atomicCAS(&a.info[ic].status, CHP_SYS_OK, CHP_SYS_NONFINITE);
+    }
+    if (a.mode == 1) {
+      for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+      if ((threadIdx.x & 31) == 0) atomic_max_nonneg(a.inc + ic, dmax);
+    }
+    gbar(grid);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
 struct NTables {
@@ -789,7 +1223,7 @@ void set_smem_attrs() {
   cudaFuncSetAttribute(k2d_row_pass<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)WCfg<N>::ROW_SMEM);
   cudaFuncSetAttribute(k2d_col_pass_b<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)WCfg<N>::COL_SMEM);
+                       (int)WCfgC<N>::COL_SMEM);
   cudaFuncSetAttribute(k2d_rowdst<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(double) * (2 * Cfg<N>::G * N + Cfg<N>::G * (Cfg<N>::T / 32))));
   cudaFuncSetAttribute(k2d_coldst<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -807,7 +1241,8 @@ cudaError_t run_linear_b(const chp_grid& g, const chp_spec& sp, int steps, int n
   const int m = g.m;
   const long long fs = (long long)m * N;
   double* buf[2] = {scratch, scratch + fs * nsys};
-  const dim3 rgrid((m + C::TR - 1) / C::TR, nsys), cgrid(N / C::TC, nsys);
+  using CC = WCfgC<N>;
+  const dim3 rgrid((m + C::TR - 1) / C::TR, nsys), cgrid(N / CC::TC, nsys);
   ColArgs ca{nullptr, fs, m, 2.0 * sp.dt, sp.b, (2.0 / N) * (2.0 / N), nt.lam, nt.wtab};
   for (int s = 0; s < steps; ++s) {
     RowArgs ra{};
@@ -821,7 +1256,7 @@ cudaError_t run_linear_b(const chp_grid& g, const chp_spec& sp, int steps, int n
     ra.out = buf[s & 1]; ra.out_stride = fs; ra.out_index = nullptr;
     k2d_row_pass<N><<<rgrid, C::THREADS, C::ROW_SMEM, st>>>(ra);
     ca.buf = buf[s & 1];
-    k2d_col_pass_b<N><<<cgrid, C::THREADS, C::COL_SMEM, st>>>(ca);
+    k2d_col_pass_b<N><<<cgrid, CC::THREADS, CC::COL_SMEM, st>>>(ca);
   }
   RowArgs ra{};
   ra.m = m; ra.dt = sp.dt; ra.c1 = g.c1; ra.info = info; ra.info_index = sys_index;
@@ -1168,6 +1603,37 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
                     long long sls, unsigned char* changed, double* inc, chp_sys_info* info,
                     const NTables& nt, cudaStream_t st) {
   const long long fs = (long long)g.m * N;
+  if (sp.scheme == CHP_LINEAR_A) {
+    // whole sweep in one cooperative persistent kernel (no host round trips)
+    Work2 W;
+    cudaError_t e = get_work(c, fs, nic, &W, st);
+    if (e != cudaSuccess) return e;
+    static int grid_blocks = 0;
+    const size_t smem = sizeof(double) * (256 / wdst::Geo<N>::L) * 2 * N + 16 * (size_t)N;
+    if (grid_blocks == 0) {
+      cudaFuncSetAttribute(k2d_coarse_coop<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2d_coarse_coop<N>, 256, smem);
+      grid_blocks = sms * (per > 0 ? per : 1);
+      if (grid_blocks > 4 * sms) grid_blocks = 4 * sms;
+    }
+    CoopArgs ca{};
+    ca.m = g.m; ca.nic = nic; ca.nsl = nsl; ca.n0 = n0; ca.n1 = n1; ca.mode = mode;
+    ca.c1 = g.c1; ca.dt = sp.dt; ca.b = sp.b; ca.tol = sp.cg_tol; ca.max_iter = sp.cg_max_iter;
+    ca.U = U; ca.F = F; ca.G = G; ca.ics = ics; ca.sls = sls;
+    ca.changed = changed; ca.inc = inc; ca.info = info;
+    ca.X = W.X; ca.Rv = W.Rv; ca.Pv = W.Pv; ca.Yv = W.Yv; ca.Cv = W.Cv; ca.CT = W.T2;
+    ca.part = W.T1;                      // >= 16 * grid doubles
+    ca.bar = reinterpret_cast<unsigned int*>(W.res);
+    cudaMemsetAsync(ca.bar, 0, sizeof(unsigned int), st);
+    ca.lam = nt.lam; ca.wtab = nt.wtab;
+    void* args[] = {&ca};
+    return cudaLaunchCooperativeKernel((void*)k2d_coarse_coop<N>, dim3(grid_blocks), dim3(256),
+                                       args, smem, st);
+  }
   // g-buffer: nic compact fields (outside the propagate workspaces)
   double* gb = nullptr;
   cudaError_t e = cudaMallocAsync(&gb, sizeof(double) * fs * nic, st);

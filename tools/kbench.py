@@ -78,3 +78,23 @@ if __name__ == "__main__":
         res.append(one_d(1025, 64, S.Scheme.LINEAR_A, 2.0 ** -5, 0.03, 1))
     for r in res:
         print(json.dumps(r), flush=True)
+
+
+def coarse_sweep(nx=1025, nsl=8):
+    """Device coarse sweep (cooperative LINEAR_A kernel): ms per slice."""
+    from paper_2304_14074_b200 import parareal as P
+    from paper_2304_14074_b200.engine import PararealEngine
+    from paper_2304_14074_b200.grid import Field
+    g = SpatialGrid(2, nx)
+    part = P.TimePartition(2.0 / 512 * nsl, nsl, 1)
+    f, c = P.propagator_pair(P.AlgorithmVariant.PA3, part, 0.01)
+    eng = PararealEngine(g, f, c, nsl, 1)
+    eng.load([Field(g, 0.1 + np.random.default_rng(0).uniform(-0.05, 0.05, g.interior_count))])
+    ms = ev_time(lambda: eng.coarse_init(), reps=2)
+    si = S.read_sysinfo(eng.info_coarse)
+    return {"what": "2D coarse sweep (mode 0)", "nx": nx, "slices": nsl, "ms": ms,
+            "ms_per_slice": ms / nsl, "cg_total": int(si["cg_total"][0])}
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "coarse":
+    print(json.dumps(coarse_sweep()), flush=True)
