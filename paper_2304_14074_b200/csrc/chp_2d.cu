@@ -90,6 +90,18 @@ CHP_DEV double w_of(double x) { return fma(x, x * x, -3.0 * x); }   // x^3 - 3x
 // ---------------------------------------------------------------------------
 // LINEAR_B row pass
 // ---------------------------------------------------------------------------
+CHP_DEV void cp_async16(void* sdst, const void* gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+CHP_DEV void cp_async8(void* sdst, const void* gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+CHP_DEV void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 template <int N>
 __global__ void __launch_bounds__(WCfg<N>::THREADS)
 k2d_row_pass(RowArgs a) {
@@ -106,34 +118,36 @@ k2d_row_pass(RowArgs a) {
   const long long fout = a.out_index ? a.out_index[s] : s;
   const double* __restrict__ in = a.in + fin * a.in_stride;
   double* __restrict__ out = a.out + fout * a.out_stride;
+  // all ROWS input rows (P, or U for the first step) in flight at once
+  for (int idx = tid; idx < C::ROWS * (N / 2); idx += C::THREADS) {
+    const int r = idx / (N / 2), jj = 2 * (idx % (N / 2));
+    const int row = i0 - 1 + r;
+    double* d = sm + (size_t)r * N + wdst::rsw(jj);
+    if (row >= 0 && row < m) cp_async16(d, in + (long long)row * N + jj);
+    else *reinterpret_cast<double2*>(d) = make_double2(0.0, 0.0);
+  }
   wdst::load_twiddles<N>(twt, a.wtab + N);
   const double2 ac = __ldg(&a.wtab[l]);
+  cp_async_wait_all();
+  __syncthreads();
   double* wr0 = sm + (size_t)(2 * g) * N;         // this group's two tile rows
   double* wr1 = wr0 + N;
   double2* scr = reinterpret_cast<double2*>(wr0);
   const int ga = i0 - 1 + 2 * g, gb = ga + 1;     // their global rows
   const bool va = ga >= 0 && ga < m, vb = gb >= 0 && gb < m;
-  const double* pa = in + (long long)(va ? ga : 0) * N;
-  const double* pb = in + (long long)(vb ? gb : 0) * N;
-  __syncthreads();
 
-  // -- phase 1: x of tile rows (2g, 2g+1) -> w = x^3 - 3x in SMEM ---------------
-  if (a.mode == ROW_FIRST) {
-    for (int j = l; j < N; j += L) {
-      wr0[wdst::rsw(j)] = va ? w_of(pa[j]) : 0.0;
-      wr1[wdst::rsw(j)] = vb ? w_of(pb[j]) : 0.0;
-    }
-  } else {
+  // -- phase 1: physical x of tile rows (2g, 2g+1), kept in SMEM --------------
+  if (a.mode != ROW_FIRST) {
     const bool last = a.mode == ROW_LAST;
     const bool ina = va && ga >= i0 && ga < i0 + C::TR;   // only inner rows are output
     const bool inb = vb && gb >= i0 && gb < i0 + C::TR;
     bool bad = false;
     auto ld = [&](int n, double& x, double& xm, double& y, double& ym) {
       const bool z0 = (n == 0);
-      x = (va && !z0) ? pa[n] : 0.0;
-      xm = (va && !z0) ? pa[N - n] : 0.0;
-      y = (vb && !z0) ? pb[n] : 0.0;
-      ym = (vb && !z0) ? pb[N - n] : 0.0;
+      x = z0 ? 0.0 : wr0[wdst::rsw(n)];
+      xm = z0 ? 0.0 : wr0[wdst::rsw(N - n)];
+      y = z0 ? 0.0 : wr1[wdst::rsw(n)];
+      ym = z0 ? 0.0 : wr1[wdst::rsw(N - n)];
     };
     auto st = [&](int k, double a2, double a21, double b2, double b21) {
       bad |= (ina && !(isfinite(a2) && isfinite(a21))) || (inb && !(isfinite(b2) && isfinite(b21)));
@@ -141,8 +155,8 @@ k2d_row_pass(RowArgs a) {
         if (ina) *reinterpret_cast<double2*>(out + (long long)ga * N + 2 * k) = make_double2(a2, a21);
         if (inb) *reinterpret_cast<double2*>(out + (long long)gb * N + 2 * k) = make_double2(b2, b21);
       } else {
-        *reinterpret_cast<double2*>(wr0 + wdst::rsw(2 * k)) = make_double2(w_of(a2), w_of(a21));
-        *reinterpret_cast<double2*>(wr1 + wdst::rsw(2 * k)) = make_double2(w_of(b2), w_of(b21));
+        *reinterpret_cast<double2*>(wr0 + wdst::rsw(2 * k)) = make_double2(a2, a21);
+        *reinterpret_cast<double2*>(wr1 + wdst::rsw(2 * k)) = make_double2(b2, b21);
       }
     };
     wdst::pair_dst<N>(ld, st, scr, twt, l, ac);
@@ -154,39 +168,30 @@ k2d_row_pass(RowArgs a) {
   }
   __syncthreads();
 
-  // -- phase 2: inner tile rows (1+2g, 2+2g) -> Q --------------------------------
-  // (L w) (FIRST: x + dt L w) into registers, block barrier, then into this
-  // group's phase-1 rows, which become the transform's input and scratch.
+  // -- phase 2: inner tile rows (1+2g, 2+2g): Q = T_j(x + dt L(x^3 - 3x)) -----
+  // rhs into registers, block barrier, then into this group's phase-1 rows,
+  // which become the transform's input and scratch.
   const bool active = g < C::GPB - 1;
   const int r0 = 1 + 2 * g;                       // tile row of the first inner row
   const int qa = i0 + 2 * g, qb = qa + 1;         // their global rows
   const bool oa = active && qa < m, ob = active && qb < m;
-  const bool first = a.mode == ROW_FIRST;
   const double c = a.c1, c4 = -4.0 * a.c1, dt = a.dt;
-  const double* qpa = in + (long long)(oa ? qa : 0) * N;
-  const double* qpb = in + (long long)(ob ? qb : 0) * N;
   constexpr int PL = N / L;                       // values per lane per row
   double la[PL], lb[PL];
-  auto lapw = [&](int r, int n) -> double {       // (L w) at tile row r, column n >= 1
-    const double* w0 = sm + (size_t)r * N;
-    const double wr = (n + 1 < N) ? w0[wdst::rsw(n + 1)] : 0.0;
-    return (((sm[(size_t)(r - 1) * N + wdst::rsw(n)] * c + w0[wdst::rsw(n - 1)] * c) +
-             w0[wdst::rsw(n)] * c4) + wr * c) + sm[(size_t)(r + 1) * N + wdst::rsw(n)] * c;
+  auto wat = [&](int r, int n) -> double {        // w = x^3 - 3x at tile row r, column n
+    return w_of(sm[(size_t)r * N + wdst::rsw(n)]);
+  };
+  auto rhs = [&](int r, int n) -> double {        // x + dt L w at tile row r, column n >= 1
+    const double wr = (n + 1 < N) ? wat(r, n + 1) : 0.0;
+    const double lw = (((wat(r - 1, n) * c + wat(r, n - 1) * c) + wat(r, n) * c4) + wr * c) +
+                      wat(r + 1, n) * c;
+    return sm[(size_t)r * N + wdst::rsw(n)] + dt * lw;
   };
 #pragma unroll
   for (int i = 0; i < PL; ++i) {
     const int n = l + L * i;
-    double x = 0.0, y = 0.0;
-    if (active && n > 0) {
-      x = lapw(r0, n);
-      y = lapw(r0 + 1, n);
-      if (first) {   // Q = T_j(x + dt L w) from the physical input
-        x = (oa ? qpa[n] : 0.0) + dt * x;
-        y = (ob ? qpb[n] : 0.0) + dt * y;
-      }
-    }
-    la[i] = x;
-    lb[i] = y;
+    la[i] = (active && n > 0) ? rhs(r0, n) : 0.0;
+    lb[i] = (active && n > 0) ? rhs(r0 + 1, n) : 0.0;
   }
   __syncthreads();
 #pragma unroll
@@ -202,23 +207,9 @@ k2d_row_pass(RowArgs a) {
     y = z0 ? 0.0 : wr1[wdst::rsw(n)];
     ym = z0 ? 0.0 : wr1[wdst::rsw(N - n)];
   };
-  const double half = 0.5 * N;
   auto st2 = [&](int k, double a2, double a21, double b2, double b21) {
-    if (first) {
-      if (oa) *reinterpret_cast<double2*>(out + (long long)qa * N + 2 * k) = make_double2(a2, a21);
-      if (ob) *reinterpret_cast<double2*>(out + (long long)qb * N + 2 * k) = make_double2(b2, b21);
-      return;
-    }
-    if (oa) {
-      const double2 p = *reinterpret_cast<const double2*>(qpa + 2 * k);
-      *reinterpret_cast<double2*>(out + (long long)qa * N + 2 * k) =
-          make_double2(k == 0 ? 0.0 : fma(half, p.x, dt * a2), fma(half, p.y, dt * a21));
-    }
-    if (ob) {
-      const double2 p = *reinterpret_cast<const double2*>(qpb + 2 * k);
-      *reinterpret_cast<double2*>(out + (long long)qb * N + 2 * k) =
-          make_double2(k == 0 ? 0.0 : fma(half, p.x, dt * b2), fma(half, p.y, dt * b21));
-    }
+    if (oa) *reinterpret_cast<double2*>(out + (long long)qa * N + 2 * k) = make_double2(a2, a21);
+    if (ob) *reinterpret_cast<double2*>(out + (long long)qb * N + 2 * k) = make_double2(b2, b21);
   };
   wdst::pair_dst<N>(ld2, st2, scr, twt, l, ac);
 }
@@ -254,11 +245,12 @@ k2d_col_pass_b(ColArgs a) {
   wdst::load_twiddles<N>(twt, a.wtab + N);
   const double2 ac = __ldg(&a.wtab[l]);
   // logical (column c, math row n) at csw(c, n)
-#pragma unroll 8
   for (int idx = tid; idx < N * TC; idx += C::THREADS) {
     const int n = idx / TC, cc = idx % TC;
-    sm[csw<N>(cc, n)] = (n > 0) ? buf[(long long)(n - 1) * N + j0 + cc] : 0.0;
+    if (n > 0) cp_async8(&sm[csw<N>(cc, n)], buf + (long long)(n - 1) * N + j0 + cc);
+    else sm[csw<N>(cc, n)] = 0.0;
   }
+  cp_async_wait_all();
   __syncthreads();
   // groups beyond the tile (small N) run on zeros so every lane of the warp
   // takes part in pair_dst's shuffles / __syncwarp
