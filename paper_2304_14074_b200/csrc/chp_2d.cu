@@ -133,14 +133,48 @@ k2d_row_pass(RowArgs a) {
   double* wr0 = sm + (size_t)(2 * g) * N;         // this group's two tile rows
   double* wr1 = wr0 + N;
   double2* scr = reinterpret_cast<double2*>(wr0);
-  const int ga = i0 - 1 + 2 * g, gb = ga + 1;     // their global rows
-  const bool va = ga >= 0 && ga < m, vb = gb >= 0 && gb < m;
-
-  // -- phase 1: physical x of tile rows (2g, 2g+1), kept in SMEM --------------
-  if (a.mode != ROW_FIRST) {
-    const bool last = a.mode == ROW_LAST;
-    const bool ina = va && ga >= i0 && ga < i0 + C::TR;   // only inner rows are output
-    const bool inb = vb && gb >= i0 && gb < i0 + C::TR;
+  const bool last = a.mode == ROW_LAST;
+  const double c = a.c1, c4 = -4.0 * a.c1, dt = a.dt;
+  constexpr int PL = N / L;                       // values per lane per row
+  // phase 0: x = T_j P of tile rows (2g, 2g+1)      (skipped for the first step)
+  // phase 1: Q = T_j(x + dt L(x^3 - 3x)) of inner tile rows (1+2g, 2+2g)
+  // One pair_dst call site for both phases keeps the kernel's code small.
+#pragma unroll 1
+  for (int ph = (a.mode == ROW_FIRST) ? 1 : 0; ph < 2; ++ph) {
+    const int ra = (ph == 0) ? i0 - 1 + 2 * g : i0 + 2 * g;     // global rows of the pair
+    const int rb = ra + 1;
+    const bool active = (ph == 0) || (g < C::GPB - 1);
+    bool oa, ob;                                                // rows this group outputs
+    if (ph == 0) {
+      oa = ra >= i0 && ra < i0 + C::TR && ra < m;
+      ob = rb >= i0 && rb < i0 + C::TR && rb < m;
+    } else {
+      oa = active && ra < m;
+      ob = active && rb < m;
+      // x + dt L w into registers, block barrier, then into this group's rows
+      double la[PL], lb[PL];
+      const int r0 = 1 + 2 * g;
+      auto wat = [&](int r, int n) -> double { return w_of(sm[(size_t)r * N + wdst::rsw(n)]); };
+      auto rhs = [&](int r, int n) -> double {
+        const double wr = (n + 1 < N) ? wat(r, n + 1) : 0.0;
+        const double lw = (((wat(r - 1, n) * c + wat(r, n - 1) * c) + wat(r, n) * c4) + wr * c) +
+                          wat(r + 1, n) * c;
+        return sm[(size_t)r * N + wdst::rsw(n)] + dt * lw;
+      };
+#pragma unroll
+      for (int i = 0; i < PL; ++i) {
+        const int n = l + L * i;
+        la[i] = (active && n > 0) ? rhs(r0, n) : 0.0;
+        lb[i] = (active && n > 0) ? rhs(r0 + 1, n) : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < PL; ++i) {
+        wr0[wdst::rsw(l + L * i)] = la[i];
+        wr1[wdst::rsw(l + L * i)] = lb[i];
+      }
+      __syncwarp();
+    }
     bool bad = false;
     auto ld = [&](int n, double& x, double& xm, double& y, double& ym) {
       const bool z0 = (n == 0);
@@ -150,68 +184,26 @@ k2d_row_pass(RowArgs a) {
       ym = z0 ? 0.0 : wr1[wdst::rsw(N - n)];
     };
     auto st = [&](int k, double a2, double a21, double b2, double b21) {
-      bad |= (ina && !(isfinite(a2) && isfinite(a21))) || (inb && !(isfinite(b2) && isfinite(b21)));
-      if (last) {
-        if (ina) *reinterpret_cast<double2*>(out + (long long)ga * N + 2 * k) = make_double2(a2, a21);
-        if (inb) *reinterpret_cast<double2*>(out + (long long)gb * N + 2 * k) = make_double2(b2, b21);
+      if (ph == 0) bad |= (oa && !(isfinite(a2) && isfinite(a21))) ||
+                          (ob && !(isfinite(b2) && isfinite(b21)));
+      if (ph == 1 || last) {
+        if (oa) *reinterpret_cast<double2*>(out + (long long)ra * N + 2 * k) = make_double2(a2, a21);
+        if (ob) *reinterpret_cast<double2*>(out + (long long)rb * N + 2 * k) = make_double2(b2, b21);
       } else {
         *reinterpret_cast<double2*>(wr0 + wdst::rsw(2 * k)) = make_double2(a2, a21);
         *reinterpret_cast<double2*>(wr1 + wdst::rsw(2 * k)) = make_double2(b2, b21);
       }
     };
     wdst::pair_dst<N>(ld, st, scr, twt, l, ac);
-    if (__syncthreads_or(bad) && tid == 0) {
-      const long long fi = a.info_index ? a.info_index[s] : s;
-      atomicCAS(&a.info[fi].status, CHP_SYS_OK, CHP_SYS_NONFINITE);
+    if (ph == 0) {
+      if (__syncthreads_or(bad) && tid == 0) {
+        const long long fi = a.info_index ? a.info_index[s] : s;
+        atomicCAS(&a.info[fi].status, CHP_SYS_OK, CHP_SYS_NONFINITE);
+      }
+      if (last) return;
     }
-    if (last) return;
+    __syncthreads();
   }
-  __syncthreads();
-
-  // -- phase 2: inner tile rows (1+2g, 2+2g): Q = T_j(x + dt L(x^3 - 3x)) -----
-  // rhs into registers, block barrier, then into this group's phase-1 rows,
-  // which become the transform's input and scratch.
-  const bool active = g < C::GPB - 1;
-  const int r0 = 1 + 2 * g;                       // tile row of the first inner row
-  const int qa = i0 + 2 * g, qb = qa + 1;         // their global rows
-  const bool oa = active && qa < m, ob = active && qb < m;
-  const double c = a.c1, c4 = -4.0 * a.c1, dt = a.dt;
-  constexpr int PL = N / L;                       // values per lane per row
-  double la[PL], lb[PL];
-  auto wat = [&](int r, int n) -> double {        // w = x^3 - 3x at tile row r, column n
-    return w_of(sm[(size_t)r * N + wdst::rsw(n)]);
-  };
-  auto rhs = [&](int r, int n) -> double {        // x + dt L w at tile row r, column n >= 1
-    const double wr = (n + 1 < N) ? wat(r, n + 1) : 0.0;
-    const double lw = (((wat(r - 1, n) * c + wat(r, n - 1) * c) + wat(r, n) * c4) + wr * c) +
-                      wat(r + 1, n) * c;
-    return sm[(size_t)r * N + wdst::rsw(n)] + dt * lw;
-  };
-#pragma unroll
-  for (int i = 0; i < PL; ++i) {
-    const int n = l + L * i;
-    la[i] = (active && n > 0) ? rhs(r0, n) : 0.0;
-    lb[i] = (active && n > 0) ? rhs(r0 + 1, n) : 0.0;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < PL; ++i) {
-    wr0[wdst::rsw(l + L * i)] = la[i];
-    wr1[wdst::rsw(l + L * i)] = lb[i];
-  }
-  __syncwarp();
-  auto ld2 = [&](int n, double& x, double& xm, double& y, double& ym) {
-    const bool z0 = (n == 0);
-    x = z0 ? 0.0 : wr0[wdst::rsw(n)];
-    xm = z0 ? 0.0 : wr0[wdst::rsw(N - n)];
-    y = z0 ? 0.0 : wr1[wdst::rsw(n)];
-    ym = z0 ? 0.0 : wr1[wdst::rsw(N - n)];
-  };
-  auto st2 = [&](int k, double a2, double a21, double b2, double b21) {
-    if (oa) *reinterpret_cast<double2*>(out + (long long)qa * N + 2 * k) = make_double2(a2, a21);
-    if (ob) *reinterpret_cast<double2*>(out + (long long)qb * N + 2 * k) = make_double2(b2, b21);
-  };
-  wdst::pair_dst<N>(ld2, st2, scr, twt, l, ac);
 }
 
 // ---------------------------------------------------------------------------
