@@ -51,6 +51,15 @@ CHP_DEV double bilap5(double ym2, double ym1, double y0, double yp1, double yp2,
 
 CHP_DEV double ld(const double* v, int i, int m) { return (i >= 0 && i < m) ? v[i] : 0.0; }
 
+// x / d correctly rounded, given r = RN(1/d): q0 = RN(x r), q = RN(q0 + (x - q0 d) r)
+// (Markstein's theorem; exactly IEEE x/d, but three dependent FMA-class ops
+// instead of the division subroutine on the sequential critical path).
+CHP_DEV double div_rn(double x, double d, double r) {
+  const double q0 = x * r;
+  const double e = fma(-q0, d, x);
+  return fma(e, r, q0);
+}
+
 // ---------------------------------------------------------------------------
 // Banded (2,2) LU with partial pivoting, LAPACK dgbtf2 + dgbtrs(L part).
 // gen(r, e[5], &rhs) produces row r of the ORIGINAL matrix, entries
@@ -79,6 +88,7 @@ CHP_DEV int band_lu_forward(int m, Gen gen, double* ub, long long ks) {
     }
   }
   int singular = 0;
+  #pragma unroll 8
   for (int j = 0; j < m; ++j) {
     const int km = min(2, m - 1 - j);
     int jp = 0;
@@ -113,10 +123,11 @@ CHP_DEV int band_lu_forward(int m, Gen gen, double* ub, long long ks) {
     } else {
       singular = 1;
     }
-    double* u = ub + (long long)j * 6 * ks;
+    double* u = ub + (long long)j * 7 * ks;
 #pragma unroll
     for (int c = 0; c < 5; ++c) u[c * ks] = W[0][c];
     u[5 * ks] = bb[0];
+    u[6 * ks] = 1.0 / W[0][0];                    // RN(1/U_jj) for the backward sweep
     // slide the window one row/column down
 #pragma unroll
     for (int c = 0; c < 4; ++c) { W[0][c] = W[1][c + 1]; W[1][c] = W[2][c + 1]; }
@@ -144,14 +155,15 @@ CHP_DEV int band_lu_forward(int m, Gen gen, double* ub, long long ks) {
 // Upper-triangular band solve (dtbsv 'U','N', bandwidth KL+KU = 4).
 CHP_DEV void band_lu_backward(int m, const double* ub, long long ks, double* x) {
   double x1 = 0.0, x2 = 0.0, x3 = 0.0, x4 = 0.0;
+  #pragma unroll 8
   for (int i = m - 1; i >= 0; --i) {
-    const double* u = ub + (long long)i * 6 * ks;
+    const double* u = ub + (long long)i * 7 * ks;
     double t = u[5 * ks];
     t = fma(-x4, u[4 * ks], t);
     t = fma(-x3, u[3 * ks], t);
     t = fma(-x2, u[2 * ks], t);
     t = fma(-x1, u[1 * ks], t);
-    const double xi = t / u[0];
+    const double xi = div_rn(t, u[0], u[6 * ks]);
     x4 = x3; x3 = x2; x2 = x1; x1 = xi;
     x[i] = xi;
   }
@@ -212,11 +224,13 @@ CHP_DEV void step_linear_b(const G1& g, double dt, const double* __restrict__ fa
   const double* F0 = fac;
   const double* F1 = fac + m;
   const double* F2 = fac + 2 * m;
+  const double* R2 = fac + 3 * m;               // RN(1 / F2[i])
   // forward: rhs_i on the fly, then U^T y = rhs (dtbsv 'U','T': dot then divide)
   double v0 = src[0];
   double w_m = 0.0;
   double w_0 = chp_cube_minus_3v(v0);
   double y1 = 0.0, y2 = 0.0;  // y_{i-1}, y_{i-2}
+  #pragma unroll 8
   for (int i = 0; i < m; ++i) {
     const double vp = (i + 1 < m) ? src[i + 1] : 0.0;
     const double w_p = (i + 1 < m) ? chp_cube_minus_3v(vp) : 0.0;
@@ -224,18 +238,19 @@ CHP_DEV void step_linear_b(const G1& g, double dt, const double* __restrict__ fa
     double dot = 0.0;
     if (i >= 2) dot = fma(y2, F0[i], dot);
     if (i >= 1) dot = fma(y1, F1[i], dot);
-    const double yi = (rhs - dot) / F2[i];
+    const double yi = div_rn(rhs - dot, F2[i], R2[i]);
     yb[(long long)i * ks] = yi;
     y2 = y1; y1 = yi;
     w_m = w_0; w_0 = w_p; v0 = vp;
   }
   // backward: U x = y (dtbsv 'U','N': divide then axpy)
   double x1 = 0.0, x2 = 0.0;
+  #pragma unroll 8
   for (int i = m - 1; i >= 0; --i) {
     double t = yb[(long long)i * ks];
     if (i + 2 < m) t = fma(-x2, F0[i + 2], t);
     if (i + 1 < m) t = fma(-x1, F1[i + 1], t);
-    const double xi = t / F2[i];
+    const double xi = div_rn(t, F2[i], R2[i]);
     x2 = x1; x1 = xi;
     dst[i] = xi;
   }
@@ -248,6 +263,7 @@ CHP_DEV int step_eyre(const G1& g, double d, double b, double tol, int maxit,
                       const double* src, double* dst, double* yh, double* ub, long long ks,
                       int* iters, double* res) {
   const int m = g.m;
+  #pragma unroll 8
   for (int i = 0; i < m; ++i) {
     const double u0 = src[i];
     yh[(long long)i * ks] = u0 - d * lap3(ld(src, i - 1, m), u0, ld(src, i + 1, m), g.c1);
@@ -263,6 +279,7 @@ CHP_DEV int step_eyre(const G1& g, double d, double b, double tol, int maxit,
     {
       double ym2 = 0.0, ym1 = 0.0, y0 = y[0], yp1 = ld(y, 1, m);
       double cm = 0.0, c0 = chp_cube(y0);
+      #pragma unroll 8
       for (int i = 0; i < m; ++i) {
         const double yp2 = ld(y, i + 2, m);
         const double cp = (i + 1 < m) ? chp_cube(yp1) : 0.0;
@@ -387,6 +404,8 @@ __global__ void k1d_pbtf2(chp_grid gg, double dt, double b, double* fac, int* er
       }
     }
   }
+  if (info == 0)
+    for (int j = 0; j < m; ++j) fac[3 * m + j] = 1.0 / A2[j];   // RN(1/U_jj)
   *err = info;
 }
 

@@ -104,7 +104,7 @@ chp_status factor_1d(chp_ctx* c, const chp_grid* g, double dt, double b, cudaStr
   auto it = c->factors.find(key);
   if (it != c->factors.end()) { *out = it->second; return CHP_OK; }
   double* fac = nullptr;
-  cudaError_t e = cudaMalloc(&fac, sizeof(double) * 3 * g->m);
+  cudaError_t e = cudaMalloc(&fac, sizeof(double) * 4 * g->m);
   if (e != cudaSuccess) return cuda_fail(c, e, "factor alloc");
   e = chp1d_factor(*g, dt, b, fac, c->dev_err, st);
   if (e != cudaSuccess) { cudaFree(fac); return cuda_fail(c, e, "factor launch"); }
@@ -192,10 +192,10 @@ chp_status chp_propagate(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int 
       if (s != CHP_OK) return s;
     }
     const size_t per = (size_t)g->m * (size_t)nsys * sizeof(double);
-    chp_status s = ensure_scratch(c, per * 8, st);
+    chp_status s = ensure_scratch(c, per * 9, st);
     if (s != CHP_OK) return s;
     double* ub = c->scratch;
-    double* yh = ub + (size_t)g->m * 6 * nsys;
+    double* yh = ub + (size_t)g->m * 7 * nsys;
     double* tmp = yh + (size_t)g->m * nsys;
     cudaError_t e = chp1d_propagate(*g, *sp, steps, nsys, in, in_stride, out, out_stride,
                                     sys_index, fac, ub, yh, tmp, info, st);
@@ -228,10 +228,10 @@ chp_status chp_coarse_sweep(chp_ctx* c, const chp_grid* g, const chp_spec* sp, i
       if (s != CHP_OK) return s;
     }
     const size_t per = (size_t)g->m * (size_t)nic * sizeof(double);
-    chp_status s = ensure_scratch(c, per * 8, st);
+    chp_status s = ensure_scratch(c, per * 9, st);
     if (s != CHP_OK) return s;
     double* ub = c->scratch;
-    double* yh = ub + (size_t)g->m * 6 * nic;
+    double* yh = ub + (size_t)g->m * 7 * nic;
     double* tmp = yh + (size_t)g->m * nic;
     cudaError_t e = chp1d_coarse_sweep(*g, *sp, mode, nic, nsl, n0, n1, U, F, G, ic_stride,
                                        sl_stride, changed, inc, fac, ub, yh, tmp, info, st);
