@@ -34,7 +34,8 @@ def run(cfg: int, max_iter=None, n_ic=None):
             "fine_slice_propagations": eng.stats.fine_systems,
             "fine_rate": eng.stats.fine_point_steps / wall,
             "newton_steps": eng.newton.steps, "newton_total": eng.newton.total_iterations,
-            "last_increments": incs[-4:, 0].tolist() if incs.size else []}
+            "last_increments": incs[-4:, 0].tolist() if incs.size else [],
+            "increments_ic0": incs[:, 0].tolist() if incs.size else []}
 
 
 if __name__ == "__main__":
