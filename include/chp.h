@@ -151,6 +151,11 @@ chp_status chp_max_abs_diff(chp_ctx* ctx, const chp_grid* g, int n_fields,
                             const double* b, long long b_stride,
                             double* out, void* stream);
 
+/* Debug: barrier timestamps (globaltimer ns) of the last cooperative 2D
+ * coarse sweep when CHP_COOP_TRACE is set in the environment; returns the
+ * number of entries copied (0 when tracing is off). */
+int chp_debug_trace(unsigned long long* host, int n);
+
 #ifdef __cplusplus
 }
 #endif

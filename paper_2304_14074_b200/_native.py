@@ -23,6 +23,7 @@ SYS_OK, SYS_NEWTON, SYS_NONFINITE, SYS_SINGULAR, SYS_CG = 0, 1, 2, 3, 4
 EXPORTS = (
     "chp_version", "chp_status_str", "chp_ctx_create", "chp_ctx_destroy", "chp_last_error",
     "chp_sysinfo_reset", "chp_propagate", "chp_coarse_sweep", "chp_max_abs_diff",
+    "chp_debug_trace",
 )
 
 
@@ -78,6 +79,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.chp_coarse_sweep.argtypes = [vp, C.POINTER(ChpGrid), C.POINTER(ChpSpec), i, i, i, i, i,
                                    vp, vp, vp, ll, ll, vp, vp, vp, vp]
     L.chp_max_abs_diff.argtypes = [vp, C.POINTER(ChpGrid), i, vp, ll, vp, ll, vp, vp]
+    L.chp_debug_trace.argtypes = [vp, i]
     for name in EXPORTS:
         if name not in ("chp_version", "chp_status_str", "chp_last_error"):
             getattr(L, name).restype = C.c_int

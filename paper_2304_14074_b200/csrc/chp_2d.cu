@@ -22,6 +22,7 @@
 #include <math.h>
 
 #include <map>
+#include <stdlib.h>
 #include <string>
 #include <vector>
 
@@ -780,6 +781,8 @@ struct CoopArgs {
   double* part;                          // [2][gridDim][8] block partials
   unsigned int* bar;                     // grid barrier counter (zeroed by the host)
   const double* lam; const double2* wtab;
+  unsigned long long* trace;             // optional: globaltimer after each barrier
+  int trace_cap, pad2_;
 };
 
 // Grid-wide barrier for the co-resident (cooperative) launch: one relaxed
@@ -787,9 +790,16 @@ struct CoopArgs {
 struct GridBar {
   unsigned int* cnt;
   unsigned int gen;
+  unsigned long long* trace;
+  int cap;
 };
 CHP_DEV void gbar(GridBar& b) {
   __syncthreads();
+  if (b.trace && blockIdx.x == 0 && threadIdx.x == 0 && (int)b.gen < b.cap) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    b.trace[b.gen] = t;
+  }
   b.gen += 1;
   if (threadIdx.x == 0) {
     __threadfence();
@@ -983,7 +993,7 @@ __device__ __noinline__ void coop_cols(CoopCtx<N>& x, const double* src, double*
 
 template <int N>
 __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
-  GridBar grid{a.bar, 0u};
+  GridBar grid{a.bar, 0u, a.trace, a.trace_cap};
   extern __shared__ __align__(16) double smc[];
   __shared__ double red[64];
   constexpr int L = wdst::Geo<N>::L;
@@ -1338,6 +1348,8 @@ __global__ void k2d_newton_commit(int nsys, const NewtonRec* rec, chp_sys_info* 
 
 }  // namespace
 
+unsigned long long* g_coop_trace = nullptr;
+
 struct Chp2d {
   std::map<int, NTables> tables;
   double* scratch = nullptr;      // LINEAR_B ping-pong fields
@@ -1612,6 +1624,14 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
     ca.X = W.X; ca.Rv = W.Rv; ca.Pv = W.Pv; ca.Yv = W.Yv; ca.Cv = W.Cv; ca.CT = W.T2;
     ca.part = W.T1;                      // >= 16 * grid doubles
     ca.bar = reinterpret_cast<unsigned int*>(W.res);
+    {
+      static unsigned long long* tr = nullptr;
+      const char* env = getenv("CHP_COOP_TRACE");
+      if (env && !tr) cudaMalloc(&tr, sizeof(unsigned long long) * 4096);
+      ca.trace = env ? tr : nullptr;
+      ca.trace_cap = 4096;
+      if (env) g_coop_trace = tr;
+    }
     cudaMemsetAsync(ca.bar, 0, sizeof(unsigned int), st);
     ca.lam = nt.lam; ca.wtab = nt.wtab;
     void* args[] = {&ca};
@@ -1702,4 +1722,12 @@ cudaError_t chp2d_coarse_sweep(Chp2d* c, const chp_grid& g, const chp_spec& sp, 
                                      sl_stride, changed, inc, info, *nt, st));
   *err = "unsupported N";
   return cudaSuccess;
+}
+
+// debug: copy the cooperative coarse kernel's barrier timestamps (ns) to the host
+extern "C" int chp_debug_trace(unsigned long long* host, int n) {
+  if (!g_coop_trace || !host || n <= 0) return 0;
+  if (n > 4096) n = 4096;
+  cudaMemcpy(host, g_coop_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
+  return n;
 }

@@ -1,6 +1,7 @@
 """Kernel micro-timings on the GPU (CUDA events): 2D LINEAR_B fine propagator,
 2D LINEAR_A PCG coarse step, 1D propagators.  Usage: python tools/kbench.py [what]"""
 import json
+import os
 import sys
 import time
 
@@ -98,3 +99,21 @@ def coarse_sweep(nx=1025, nsl=8):
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "coarse":
     print(json.dumps(coarse_sweep()), flush=True)
+
+
+def coarse_trace(nx=1025, nsl=4):
+    """Per-phase timeline of the cooperative coarse kernel (CHP_COOP_TRACE=1)."""
+    import ctypes
+    os.environ["CHP_COOP_TRACE"] = "1"
+    from paper_2304_14074_b200 import _native as NN
+    r = coarse_sweep(nx, nsl)
+    buf = (ctypes.c_ulonglong * 4096)()
+    n = NN.lib().chp_debug_trace(buf, 4096)
+    ts = np.array(buf[:n], dtype=np.int64)
+    ts = ts[ts > 0]
+    d = np.diff(ts) / 1e3
+    return {"coarse": r, "barriers": int(ts.size), "phase_us": [round(x, 1) for x in d[:80]]}
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace":
+    print(json.dumps(coarse_trace()), flush=True)
