@@ -247,6 +247,11 @@ def run_gpu(args):
             dist.destroy_process_group()
         return
     peaks, src = measured_peaks()
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            traffic = json.load(f)["fine_step_bytes_per_grid_point_step"]
+    except (OSError, KeyError, ValueError):
+        traffic = None
     local_pts = eng.local_slices * CFG["J"] * g.interior_count
     fine_bytes = 32.0 * local_pts          # algorithmic HBM bytes of the fine sweep
     achieved = fine_bytes / (fine_ms * 1e-3) / 1e9
@@ -264,7 +269,8 @@ def run_gpu(args):
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                      "peak_source": src,
                      "kernel": "LINEAR_B fine propagator (k2d_row_pass + k2d_col_pass_b), "
-                               "32 B/grid-point-step", "traffic": None},
+                               "32 B/grid-point-step", "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per grid-point-step (ncu, row+column pass)"},
         "clocks": clocks, "gpu_launches": launches * args.steps if launches else launches,
         "launches_per_step": names,
         "e2e": e2e,
