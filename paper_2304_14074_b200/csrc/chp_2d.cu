@@ -49,24 +49,26 @@ template <int N> struct Cfg {
 // configuration of the register-resident (wdst) LINEAR_B passes
 template <int N> struct WCfg {
   static constexpr int L = wdst::Geo<N>::L;
-  static constexpr int WARPS = (N >= 64) ? 8 : 1;
+  static constexpr int WARPS = (N >= 1024) ? 8 * (L / 32) : ((N >= 64) ? 8 : 1);
   static constexpr int THREADS = WARPS * 32;
   static constexpr int GPB = THREADS / L;          // lane groups (pairs) per block
   static constexpr int ROWS = 2 * GPB;             // rows held per row tile (incl. halo)
   static constexpr int TR = ROWS - 2;              // inner rows per row tile
   static constexpr int TC = (2 * GPB < N) ? 2 * GPB : N;   // columns per column tile
-  static constexpr size_t ROW_SMEM = sizeof(double) * (size_t)ROWS * N + 16 * (size_t)N;
+  static constexpr int MINB = (N <= 256) ? 2 : 1;          // blocks/SM the registers allow
+  static constexpr size_t ROW_SMEM = sizeof(double) * (size_t)ROWS * N + 16 * (size_t)(N + 64);
   static constexpr size_t COL_SMEM = sizeof(double) * (size_t)(2 * GPB) * N + 16 * (size_t)N;
 };
 
 // column pass: smaller blocks (no halo), so that two blocks overlap on an SM
 template <int N> struct WCfgC {
   static constexpr int L = wdst::Geo<N>::L;
-  static constexpr int WARPS = (N >= 64) ? 4 : 1;
+  static constexpr int WARPS = (N >= 1024) ? 4 * (L / 32) : ((N >= 64) ? 4 : 1);
+  static constexpr int MINB = (N <= 256) ? 4 : 2;
   static constexpr int THREADS = WARPS * 32;
   static constexpr int GPB = THREADS / L;
   static constexpr int TC = (2 * GPB < N) ? 2 * GPB : N;
-  static constexpr size_t COL_SMEM = sizeof(double) * (size_t)(2 * GPB) * N + 16 * (size_t)N;
+  static constexpr size_t COL_SMEM = sizeof(double) * (size_t)(2 * GPB) * N + 16 * (size_t)(N + 64);
 };
 
 enum RowMode { ROW_FIRST = 0, ROW_MID = 1, ROW_LAST = 2 };
@@ -104,7 +106,7 @@ CHP_DEV void cp_async_wait_all() {
 }
 
 template <int N>
-__global__ void __launch_bounds__(WCfg<N>::THREADS)
+__global__ void __launch_bounds__(WCfg<N>::THREADS, WCfg<N>::MINB)
 k2d_row_pass(RowArgs a) {
   using C = WCfg<N>;
   constexpr int L = C::L;
@@ -174,7 +176,7 @@ k2d_row_pass(RowArgs a) {
         wr0[wdst::rsw(l + L * i)] = la[i];
         wr1[wdst::rsw(l + L * i)] = lb[i];
       }
-      __syncwarp();
+      wdst::group_sync<N>();
     }
     bool bad = false;
     auto ld = [&](int n, double& x, double& xm, double& y, double& ym) {
@@ -223,7 +225,7 @@ template <int N>
 CHP_DEV int csw(int c, int n) { return c * N + (n ^ c ^ (((n >> 5) & 15) << 1)); }
 
 template <int N>
-__global__ void __launch_bounds__(WCfgC<N>::THREADS, 2)
+__global__ void __launch_bounds__(WCfgC<N>::THREADS, WCfgC<N>::MINB)
 k2d_col_pass_b(ColArgs a) {
   using C = WCfgC<N>;
   constexpr int L = C::L, TC = C::TC;
@@ -281,7 +283,7 @@ k2d_col_pass_b(ColArgs a) {
   for (int pass = 0; pass < 2; ++pass) {
     scale_pass = (pass == 0);
     wdst::pair_dst<N>(ld, st, scr, twt, l, ac);
-    __syncwarp();
+    wdst::group_sync<N>();
   }
   __syncthreads();
 #pragma unroll 8
@@ -864,8 +866,18 @@ CHP_DEV void coop_total(const double* part, double* red, double (&out)[K]) {
 // row-pair DST over the field: dst rows = T_j src rows (+ optional CG op)
 //   op 0: dst = T_j src
 //   op 1: dst = d .* p + T_j src ; returns thread partial of p.q
+//   op 2: CG direction update fused in: src = P is replaced by
+//         P = R / M + beta P (M = d + acbar) before the transform
 template <int N>
-__device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, double* dst, int op, const double* p) {
+CHP_DEV double coop_zinv(const CoopArgs& a, int r, int n, double acbar) {
+  const double kap = -(a.lam[r + 1] + a.lam[n]);
+  return wdst::rcp((wdst::rcp(kap) + a.b * kap) + acbar);
+}
+
+template <int N>
+__device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, double* dst, int op,
+                                         const double* p, double beta = 0.0, double acbar = 0.0,
+                                         double* dst2 = nullptr, const double* Rv = nullptr) {
   const auto& a = x.a;
   const int m = a.m;
   double part = 0.0;
@@ -882,6 +894,23 @@ __device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, doubl
     const double* sb = src + (long long)(vb ? rb : ra) * N;
     auto ld = [&](int n, double& u, double& um, double& v, double& vm) {
       const bool z = n == 0 || !have;
+      if (op == 2) {
+        // p = r/M + beta p at (ra, n), (ra, N-n), (rb, n), (rb, N-n); the
+        // primary index n writes P back (each point has exactly one primary)
+        const long long oa = (long long)ra * N, ob = (long long)rb * N;
+        auto pn = [&](long long o, int r, int nn) {
+          return fma(beta, src[o + nn], Rv[o + nn] * coop_zinv<N>(a, r, nn, acbar));
+        };
+        u = z ? 0.0 : pn(oa, ra, n);
+        um = z ? 0.0 : pn(oa, ra, N - n);
+        v = (z || !vb) ? 0.0 : pn(ob, rb, n);
+        vm = (z || !vb) ? 0.0 : pn(ob, rb, N - n);
+        if (!z) {                     // new direction into the other P buffer
+          dst2[oa + n] = u;
+          if (vb) dst2[ob + n] = v;
+        }
+        return;
+      }
       u = z ? 0.0 : sa[n];
       um = z ? 0.0 : sa[N - n];
       v = (z || !vb) ? 0.0 : sb[n];
@@ -910,7 +939,7 @@ __device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, doubl
       }
     };
     wdst::pair_dst<N>(ld, st, scr, x.twt, x.l, x.ac);
-    __syncwarp();
+    wdst::group_sync<N>();
   }
   return part;
 }
@@ -925,7 +954,7 @@ __device__ __noinline__ void coop_cols(CoopCtx<N>& x, const double* src, double*
   // Block-tiled column pass: TC = 2*gpb columns per tile, coalesced tile
   // load/store through shared memory (swizzle csw), one lane group per pair.
   //   op 0: dst = scale * T_i src
-  //   op 1: dst = T_i ((scale * c) .* T_i src)   (cT: c transposed, [q][n])
+  //   op 1: dst = T_i ((scale * c) .* T_i src)   (cT: c transposed, [q-1][n])
   //   op 2: dst = T_i src .* (scale / kappa)
   const auto& a = x.a;
   const int m = a.m;
@@ -954,8 +983,9 @@ __device__ __noinline__ void coop_cols(CoopCtx<N>& x, const double* src, double*
       if (!act) return;
       const int p0 = 2 * k, p1 = p0 + 1;
       if (op == 1 && pass == 0) {
-        const double2 c_a = *reinterpret_cast<const double2*>(cT + (long long)qa * N + p0);
-        const double2 c_b = *reinterpret_cast<const double2*>(cT + (long long)qb * N + p0);
+        // column qa = 0 is the pad (its outputs are zeroed below)
+        const double2 c_a = *reinterpret_cast<const double2*>(cT + (long long)(qa > 0 ? qa - 1 : 0) * N + p0);
+        const double2 c_b = *reinterpret_cast<const double2*>(cT + (long long)(qb - 1) * N + p0);
         a2 *= scale * c_a.x; a21 *= scale * c_a.y;
         b2 *= scale * c_b.x; b21 *= scale * c_b.y;
       } else if (op == 0) {
@@ -974,11 +1004,11 @@ __device__ __noinline__ void coop_cols(CoopCtx<N>& x, const double* src, double*
     // every group runs (small N: several groups share a warp); groups beyond
     // the tile read zeros and store nothing
     wdst::pair_dst<N>(ld, st, scr, x.twt, x.l, x.ac);
-    __syncwarp();
+    wdst::group_sync<N>();
     if (op == 1) {
       pass = 1;
       wdst::pair_dst<N>(ld, st, scr, x.twt, x.l, x.ac);
-      __syncwarp();
+      wdst::group_sync<N>();
     }
     __syncthreads();
 #pragma unroll 8
@@ -1063,10 +1093,10 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
         double tc[1];
         coop_total<1>(pbuf, red, tc);
         const double acbar = a.dt * (tc[0] / ((double)m * m));
-        // c transposed for the column phases: CT[q][n] = c[n-1][q]
+        // c transposed for the column phases: CT[q-1][n] = c[n-1][q], q, n = 1..m
         for (long long t = gtid; t < tot; t += gstride) {
-          const int q = (int)(t / N), nn = (int)(t % N);
-          CT[t] = (nn > 0 && q > 0) ? Cv[(long long)(nn - 1) * N + q] : 0.0;
+          const int q1 = (int)(t / N), nn = (int)(t % N);
+          CT[t] = (nn > 0) ? Cv[(long long)(nn - 1) * N + q1 + 1] : 0.0;
         }
         // ---- b^ = (2/N)/kappa .* T_i T_j rhs -> Rv -----------------------------
         coop_rows<N>(x, Yv, Yv, 0, nullptr);
@@ -1080,10 +1110,8 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
           X[t] = 0.0;
           double z = 0.0;
           if (j > 0) {
-            const double kap = -(a.lam[i + 1] + a.lam[j]);
-            const double M = (1.0 / kap + a.b * kap) + acbar;
             const double rv = Rv[t];
-            z = rv / M;
+            z = rv * coop_zinv<N>(a, i, j, acbar);
             pr[0] = fma(rv, z, pr[0]);
             pr[1] = fma(rv, rv, pr[1]);
           }
@@ -1099,13 +1127,21 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
         int it = 0;
         bool fail = false;
         bool done = !(rr0 > 0.0);
+        double beta = 0.0;
+        double* Pc = Pv;                     // current direction; Cv is free after CT
+        double* Pn = Cv;
         while (!done) {
-          coop_rows<N>(x, Pv, Yv, 0, nullptr);
+          if (it == 0) {
+            coop_rows<N>(x, Pc, Yv, 0, nullptr);
+          } else {
+            coop_rows<N>(x, Pc, Yv, 2, nullptr, beta, acbar, Pn, Rv);
+            double* t = Pc; Pc = Pn; Pn = t;
+          }
           gbar(grid);
           coop_cols<N>(x, Yv, Yv, 1, a.dt * s2, CT);
           gbar(grid);
           double pq[1];
-          pq[0] = coop_rows<N>(x, Yv, Yv, 1, Pv);
+          pq[0] = coop_rows<N>(x, Yv, Yv, 1, Pc);
           pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
           coop_block_partials<1>(pq, red, pbuf);
           gbar(grid);
@@ -1116,12 +1152,10 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
           for (long long t = gtid; t < tot; t += gstride) {
             const int i = (int)(t / N), j = (int)(t % N);
             if (j == 0) continue;
-            X[t] = fma(alpha, Pv[t], X[t]);
+            X[t] = fma(alpha, Pc[t], X[t]);
             const double rv = fma(-alpha, Yv[t], Rv[t]);
             Rv[t] = rv;
-            const double kap = -(a.lam[i + 1] + a.lam[j]);
-            const double M = (1.0 / kap + a.b * kap) + acbar;
-            rz[0] = fma(rv, rv / M, rz[0]);
+            rz[0] = fma(rv, rv * coop_zinv<N>(a, i, j, acbar), rz[0]);
             rz[1] = fma(rv, rv, rz[1]);
           }
           pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
@@ -1129,21 +1163,13 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
           gbar(grid);
           double t1[2];
           coop_total<2>(pbuf, red, t1);
-          const double beta = t1[0] / rho;
+          beta = t1[0] / rho;
           rho = t1[0];
           ++it;
           if (!(t1[1] > tol2 * rr0)) done = true;
           else if (it >= a.max_iter) { done = true; fail = true; }
           if (!isfinite(t1[1])) { done = true; fail = true; }
           if (done) break;
-          for (long long t = gtid; t < tot; t += gstride) {
-            const int i = (int)(t / N), j = (int)(t % N);
-            if (j == 0) continue;
-            const double kap = -(a.lam[i + 1] + a.lam[j]);
-            const double M = (1.0 / kap + a.b * kap) + acbar;
-            Pv[t] = fma(beta, Pv[t], Rv[t] / M);
-          }
-          gbar(grid);
         }
         if (gtid == 0) {
           a.info[ic].cg_total += it;
@@ -1208,6 +1234,7 @@ struct Work2 {            // device workspace for one solve batch
   int* act;               // nsys
   double* res;            // nsys
   double* gbuf;           // coarse: nsys fields
+  double* coop;           // cooperative coarse sweep: block partials (16 per block)
 };
 
 template <int N>
@@ -1399,10 +1426,13 @@ cudaError_t get_tables(Chp2d* c, int N, const NTables** out) {
     const long double sp = sinl(pi * p / (2.0L * N));
     lam[p] = (double)(-4.0L / (h * h) * sp * sp);
   }
-  std::vector<double2> wt(2 * N);
-  int wl = 2;                                  // lanes of the wdst geometry for N
-  while (wl * wl * 2 <= N && wl < 32) wl *= 2;  // 8->2 16->4 32->4 64->8 ... 1024->32
-  if (wl * wl > N) wl /= 2;
+  std::vector<double2> wt(2 * N + 64);
+  // lanes of the wdst geometry for N (wdst::Geo)
+  const int wl = N == 8 ? 2 : N <= 32 ? 4 : N <= 128 ? 8 : N <= 512 ? 16 : wdst::Geo<1024>::L;
+  for (int k = 0; k < 64; ++k) {
+    const long double ang = 2.0L * pi * k / 64;
+    wt[2 * N + k] = make_double2((double)cosl(ang), (double)-sinl(ang));
+  }
   for (int l = 0; l < N; ++l)
     wt[l] = make_double2((double)cosl(pi * l / N), (double)sinl(pi * l / N));
   for (int k2 = 0; k2 < N / wl; ++k2)
@@ -1412,8 +1442,8 @@ cudaError_t get_tables(Chp2d* c, int N, const NTables** out) {
     }
   NTables t;
   cudaError_t e;
-  if ((e = cudaMalloc(&t.wtab, sizeof(double2) * 2 * N)) != cudaSuccess) return e;
-  cudaMemcpy(t.wtab, wt.data(), sizeof(double2) * 2 * N, cudaMemcpyHostToDevice);
+  if ((e = cudaMalloc(&t.wtab, sizeof(double2) * (2 * N + 64))) != cudaSuccess) return e;
+  cudaMemcpy(t.wtab, wt.data(), sizeof(double2) * (2 * N + 64), cudaMemcpyHostToDevice);
   if ((e = cudaMalloc(&t.tw, sizeof(double2) * N)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.sj, sizeof(double) * (N + 1))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.lam, sizeof(double) * N)) != cudaSuccess) return e;
@@ -1452,12 +1482,16 @@ cudaError_t host_bufs(Chp2d* c, int n) {
 }
 
 // Carve the PCG/Newton workspace for nsys systems (+ nic coarse buffers).
-cudaError_t get_work(Chp2d* c, long long fs, int nsys, Work2* W, cudaStream_t st) {
+cudaError_t get_work(Chp2d* c, long long fs, int nsys, Work2* W, cudaStream_t st,
+                     size_t coop_doubles = 0) {
   const size_t fields = 10;
   const size_t bytes = sizeof(double) * fs * nsys * fields + sizeof(double) * nsys * kPB * 4 +
-                       sizeof(CgSys) * nsys + sizeof(int) * nsys + sizeof(double) * nsys + 1024;
+                       sizeof(CgSys) * nsys + sizeof(int) * nsys + sizeof(double) * nsys + 1024 +
+                       sizeof(double) * coop_doubles;
   cudaError_t e = grow(&c->work, &c->work_bytes, bytes, st);
   if (e != cudaSuccess) return e;
+  static const bool poison = getenv("CHP_POISON") != nullptr;   // debug: NaN-fill workspaces
+  if (poison) cudaMemsetAsync(c->work, 0xFF, c->work_bytes, st);
   double* b = static_cast<double*>(c->work);
   const long long F = fs * nsys;
   W->X = b; W->Rv = b + F; W->Pv = b + 2 * F; W->Yv = b + 3 * F; W->Cv = b + 4 * F;
@@ -1467,6 +1501,7 @@ cudaError_t get_work(Chp2d* c, long long fs, int nsys, Work2* W, cudaStream_t st
   W->cg = reinterpret_cast<CgSys*>(W->partial + (long long)nsys * kPB * 4);
   W->act = reinterpret_cast<int*>(W->cg + nsys);
   W->res = reinterpret_cast<double*>(((uintptr_t)(W->act + nsys) + 15) & ~(uintptr_t)15);
+  W->coop = W->res + nsys + 2;             // cooperative sweep: barrier word + block partials
   return host_bufs(c, nsys);
 }
 
@@ -1601,11 +1636,8 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
   const long long fs = (long long)g.m * N;
   if (sp.scheme == CHP_LINEAR_A) {
     // whole sweep in one cooperative persistent kernel (no host round trips)
-    Work2 W;
-    cudaError_t e = get_work(c, fs, nic, &W, st);
-    if (e != cudaSuccess) return e;
     static int grid_blocks = 0;
-    const size_t smem = sizeof(double) * (256 / wdst::Geo<N>::L) * 2 * N + 16 * (size_t)N;
+    const size_t smem = sizeof(double) * (256 / wdst::Geo<N>::L) * 2 * N + 16 * (size_t)(N + 64);
     if (grid_blocks == 0) {
       cudaFuncSetAttribute(k2d_coarse_coop<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
@@ -1616,13 +1648,16 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
       grid_blocks = sms * (per > 0 ? per : 1);
       if (grid_blocks > 4 * sms) grid_blocks = 4 * sms;
     }
+    Work2 W;
+    cudaError_t e = get_work(c, fs, nic, &W, st, 16 * (size_t)grid_blocks + 8);
+    if (e != cudaSuccess) return e;
     CoopArgs ca{};
     ca.m = g.m; ca.nic = nic; ca.nsl = nsl; ca.n0 = n0; ca.n1 = n1; ca.mode = mode;
     ca.c1 = g.c1; ca.dt = sp.dt; ca.b = sp.b; ca.tol = sp.cg_tol; ca.max_iter = sp.cg_max_iter;
     ca.U = U; ca.F = F; ca.G = G; ca.ics = ics; ca.sls = sls;
     ca.changed = changed; ca.inc = inc; ca.info = info;
     ca.X = W.X; ca.Rv = W.Rv; ca.Pv = W.Pv; ca.Yv = W.Yv; ca.Cv = W.Cv; ca.CT = W.T2;
-    ca.part = W.T1;                      // >= 16 * grid doubles
+    ca.part = W.coop;                    // 2 x 8 doubles per block (alternating)
     ca.bar = reinterpret_cast<unsigned int*>(W.res);
     {
       static unsigned long long* tr = nullptr;

@@ -39,7 +39,10 @@ template <> struct Geo<64>   { static constexpr int L = 8,  R = 8;  };
 template <> struct Geo<128>  { static constexpr int L = 8,  R = 16; };
 template <> struct Geo<256>  { static constexpr int L = 16, R = 16; };
 template <> struct Geo<512>  { static constexpr int L = 16, R = 32; };
-template <> struct Geo<1024> { static constexpr int L = 32, R = 32; };
+#ifndef CHP_L1024
+#define CHP_L1024 32
+#endif
+template <> struct Geo<1024> { static constexpr int L = CHP_L1024, R = 1024 / CHP_L1024; };  // 64: two warps per pair
 
 CHP_DEV constexpr int brev(int k, int bits) {
   int r = 0;
@@ -96,9 +99,113 @@ CHP_DEV int zsw(int k) {
 CHP_DEV int rsw(int e) { return e ^ (((e >> 5) & 15) << 1); }
 
 // Twiddle table W_N^{l k2} laid out [k2][l] (R*L = N double2), built on the host.
+// plus W_64^k (k < 64) at twt[N + k] for the 64-lane (N = 1024) second stage
 template <int N>
 CHP_DEV void load_twiddles(double2* twt, const double2* __restrict__ g) {
-  for (int i = threadIdx.x; i < N; i += blockDim.x) twt[i] = __ldg(&g[i]);
+  for (int i = threadIdx.x; i < N + 64; i += blockDim.x) twt[i] = __ldg(&g[i]);
+}
+
+// named barrier of one 64-thread lane group (two warps)
+CHP_DEV void group_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+// synchronise one lane group (a warp or part of one; two warps for N = 1024)
+template <int N>
+CHP_DEV void group_sync() {
+  if constexpr (Geo<N>::L == 64) group_bar(1 + (int)(threadIdx.x / 64));
+  else __syncwarp();
+}
+
+// N = 1024 with 64-lane groups: R = 16 complex per lane, three register stages
+// (16-point, 4 x 4-point, 16-point) and two swizzled shared-memory transposes;
+// half the registers per lane of a 32 x 32 split, so twice the warps per SM.
+template <int N, class In, class Out>
+CHP_DEV void pair_dst64(In in, Out out, double2* scr, const double2* twt, int l, double2 ac) {
+  constexpr int L = 64, R = 16, C = N / 2 / L;
+  static_assert(N == 1024, "pair_dst64 is the N = 1024 geometry");
+  const int bar = 1 + (int)(threadIdx.x / L);
+  double2 z[R];
+#pragma unroll
+  for (int n2 = 0; n2 < R; ++n2) {
+    double a, am, b, bm;
+    in(l + L * n2, a, am, b, bm);
+    const double s = fma(ac.y, c64(n2 * (32 / R)), ac.x * s64(n2 * (32 / R)));
+    const double sa = s * (a + am), da = 0.5 * (a - am);
+    const double sb = s * (b + bm), db = 0.5 * (b - bm);
+    z[n2] = make_double2(sa + da, sb + db);
+  }
+  dft<R>(z);
+#pragma unroll
+  for (int k2 = 1; k2 < R; ++k2) z[brev(k2, 4)] = cmul(z[brev(k2, 4)], twt[k2 * L + l]);
+  group_bar(bar);
+#pragma unroll
+  for (int k2 = 0; k2 < R; ++k2) scr[k2 * L + (l ^ k2)] = z[brev(k2, 4)];
+  group_bar(bar);
+  // stage 2a: lane -> (k2 = l >> 2, la = 4 (l & 3) + t), 4-point DFTs over lb
+  const int k2 = l >> 2, q = l & 3;
+  double2 v[4][4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+#pragma unroll
+    for (int lb = 0; lb < 4; ++lb) v[t][lb] = scr[k2 * L + ((4 * q + t + 16 * lb) ^ k2)];
+  }
+  group_bar(bar);
+  const double2* w64 = twt + N;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    dft<4>(v[t]);
+#pragma unroll
+    for (int k1a = 1; k1a < 4; ++k1a)
+      v[t][brev(k1a, 2)] = cmul(v[t][brev(k1a, 2)], w64[((4 * q + t) * k1a) & 63]);
+#pragma unroll
+    for (int k1a = 0; k1a < 4; ++k1a)
+      scr[k2 * L + ((4 * (4 * q + t) + k1a) ^ k2)] = v[t][brev(k1a, 2)];
+  }
+  group_bar(bar);
+  // stage 2b: lane -> (k2 = l >> 2, k1a = l & 3), 16-point DFT over la
+  const int k1a = l & 3;
+  double2 w[16];
+#pragma unroll
+  for (int la = 0; la < 16; ++la) w[la] = scr[k2 * L + ((4 * la + k1a) ^ k2)];
+  group_bar(bar);
+  dft<16>(w);
+#pragma unroll
+  for (int k1b = 0; k1b < 16; ++k1b) scr[zsw<N>(k2 + 16 * k1a + 64 * k1b)] = w[brev(k1b, 4)];
+  group_bar(bar);
+  // post-processing on the chunk [l*C, l*C + C)
+  double ea[C], eb[C], ca[C], cb[C];
+  double sa = 0.0, sb = 0.0;
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int k = l * C + j;
+    const double2 X = scr[zsw<N>(k)];
+    const double2 Y = scr[zsw<N>((N - k) & (N - 1))];
+    ea[j] = 0.5 * (Y.y - X.y);
+    eb[j] = 0.5 * (X.x - Y.x);
+    double xa = 0.5 * (X.x + Y.x);
+    double xb = 0.5 * (X.y + Y.y);
+    if (j == 0 && l == 0) { xa *= 0.5; xb *= 0.5; ea[0] = 0.0; eb[0] = 0.0; }
+    sa += xa;
+    sb += xb;
+    ca[j] = sa;
+    cb[j] = sb;
+  }
+  // exclusive scan of the chunk totals over the 64 lanes (fixed order)
+  double ia = sa, ib = sb;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ya = __shfl_up_sync(0xffffffffu, ia, o);
+    const double yb = __shfl_up_sync(0xffffffffu, ib, o);
+    if ((l & 31) >= o) { ia += ya; ib += yb; }
+  }
+  group_bar(bar);                                    // scr reads done
+  double* tot = reinterpret_cast<double*>(scr);
+  if (l == 31) { tot[0] = ia; tot[1] = ib; }
+  group_bar(bar);
+  if (l >= 32) { ia += tot[0]; ib += tot[1]; }
+  const double offa = ia - sa, offb = ib - sb;
+  group_bar(bar);                                    // before out() may write scr
+#pragma unroll
+  for (int j = 0; j < C; ++j) out(l * C + j, ea[j], ca[j] + offa, eb[j], cb[j] + offb);
 }
 
 // Unnormalised DST-I of the pair (a, b).
@@ -111,6 +218,10 @@ CHP_DEV void load_twiddles(double2* twt, const double2* __restrict__ g) {
 //   twt: block-shared twiddle table; ac = (cos, sin)(pi l / N).
 template <int N, class In, class Out>
 CHP_DEV void pair_dst(In in, Out out, double2* scr, const double2* twt, int l, double2 ac) {
+  if constexpr (Geo<N>::L == 64) {
+    pair_dst64<N>(in, out, scr, twt, l, ac);
+    return;
+  } else {
   constexpr int L = Geo<N>::L, R = Geo<N>::R, Q = R / L;
   constexpr int LB = ilog2(L), RB = ilog2(R);
   constexpr int C = N / 2 / L;
@@ -177,6 +288,7 @@ CHP_DEV void pair_dst(In in, Out out, double2* scr, const double2* twt, int l, d
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < C; ++j) out(l * C + j, ea[j], ca[j] + offa, eb[j], cb[j] + offb);
+  }
 }
 
 // fast reciprocal: float seed + two Newton steps (relative error ~1e-16)

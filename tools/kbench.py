@@ -117,3 +117,29 @@ def coarse_trace(nx=1025, nsl=4):
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace":
     print(json.dumps(coarse_trace()), flush=True)
+
+
+def kernel_split(nx=1025, nsys=64, steps=16):
+    """Per-kernel average device time (torch profiler) of the LINEAR_B propagation."""
+    from torch.profiler import profile, ProfilerActivity
+    g = SpatialGrid(2, nx)
+    src = fields(g, nsys, base=0.1)
+    out = torch.empty_like(src)
+    spec = S.PropagatorSpec(S.Scheme.LINEAR_B, 2.0 / 512 / 256, 0.01)
+    S.propagate_batch(g, spec, steps, src, out)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        S.propagate_batch(g, spec, steps, src, out)
+        torch.cuda.synchronize()
+    agg = {}
+    for e in prof.events():
+        if e.device_type.name == "CUDA":
+            k = e.name[:60]
+            t, c = agg.get(k, (0.0, 0))
+            agg[k] = (t + e.device_time, c + 1)
+    return {k: {"us_avg": round(t / c, 1), "n": c} for k, (t, c) in agg.items()}
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "split":
+    print(json.dumps(kernel_split()), flush=True)
+    print(json.dumps(kernel_split(257, 64, 64)), flush=True)
