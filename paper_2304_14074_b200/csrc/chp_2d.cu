@@ -154,21 +154,40 @@ k2d_row_pass(RowArgs a) {
     } else {
       oa = active && ra < m;
       ob = active && rb < m;
-      // x + dt L w into registers, block barrier, then into this group's rows
+      // rhs = x + dt L w, w = x^3 - 3x: centre x into registers, then w in
+      // place over the whole tile (one cube per point), the 5-point stencil
+      // of w, and finally the rhs into this group's rows
       double la[PL], lb[PL];
       const int r0 = 1 + 2 * g;
-      auto wat = [&](int r, int n) -> double { return w_of(sm[(size_t)r * N + wdst::rsw(n)]); };
-      auto rhs = [&](int r, int n) -> double {
+#pragma unroll
+      for (int i = 0; i < PL; ++i) {
+        const int n = l + L * i;
+        la[i] = active ? sm[(size_t)r0 * N + wdst::rsw(n)] : 0.0;
+        lb[i] = active ? sm[(size_t)(r0 + 1) * N + wdst::rsw(n)] : 0.0;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < C::ROWS * N / 2; idx += C::THREADS) {
+        double2* p2 = reinterpret_cast<double2*>(sm) + idx;   // rsw keeps (2k, 2k+1) pairs
+        const double2 v = *p2;
+        *p2 = make_double2(w_of(v.x), w_of(v.y));
+      }
+      __syncthreads();
+      auto wat = [&](int r, int n) -> double { return sm[(size_t)r * N + wdst::rsw(n)]; };
+      auto lw = [&](int r, int n) -> double {
         const double wr = (n + 1 < N) ? wat(r, n + 1) : 0.0;
-        const double lw = (((wat(r - 1, n) * c + wat(r, n - 1) * c) + wat(r, n) * c4) + wr * c) +
-                          wat(r + 1, n) * c;
-        return sm[(size_t)r * N + wdst::rsw(n)] + dt * lw;
+        return (((wat(r - 1, n) * c + wat(r, n - 1) * c) + wat(r, n) * c4) + wr * c) +
+               wat(r + 1, n) * c;
       };
 #pragma unroll
       for (int i = 0; i < PL; ++i) {
         const int n = l + L * i;
-        la[i] = (active && n > 0) ? rhs(r0, n) : 0.0;
-        lb[i] = (active && n > 0) ? rhs(r0 + 1, n) : 0.0;
+        if (active && n > 0) {
+          la[i] = la[i] + dt * lw(r0, n);
+          lb[i] = lb[i] + dt * lw(r0 + 1, n);
+        } else {
+          la[i] = 0.0;
+          lb[i] = 0.0;
+        }
       }
       __syncthreads();
 #pragma unroll
@@ -178,7 +197,7 @@ k2d_row_pass(RowArgs a) {
       }
       wdst::group_sync<N>();
     }
-    bool bad = false;
+    double fin = 0.0;
     auto ld = [&](int n, double& x, double& xm, double& y, double& ym) {
       const bool z0 = (n == 0);
       x = z0 ? 0.0 : wr0[wdst::rsw(n)];
@@ -187,8 +206,10 @@ k2d_row_pass(RowArgs a) {
       ym = z0 ? 0.0 : wr1[wdst::rsw(N - n)];
     };
     auto st = [&](int k, double a2, double a21, double b2, double b21) {
-      if (ph == 0) bad |= (oa && !(isfinite(a2) && isfinite(a21))) ||
-                          (ob && !(isfinite(b2) && isfinite(b21)));
+      if (last) {                      // x * 0 is 0 unless x is NaN/Inf
+        if (oa) fin = fma(a2, 0.0, fma(a21, 0.0, fin));
+        if (ob) fin = fma(b2, 0.0, fma(b21, 0.0, fin));
+      }
       if (ph == 1 || last) {
         if (oa) *reinterpret_cast<double2*>(out + (long long)ra * N + 2 * k) = make_double2(a2, a21);
         if (ob) *reinterpret_cast<double2*>(out + (long long)rb * N + 2 * k) = make_double2(b2, b21);
@@ -198,8 +219,8 @@ k2d_row_pass(RowArgs a) {
       }
     };
     wdst::pair_dst<N>(ld, st, scr, twt, l, ac);
-    if (ph == 0) {
-      if (__syncthreads_or(bad) && tid == 0) {
+    if (last) {
+      if (__syncthreads_or(fin != 0.0) && tid == 0) {
         const long long fi = a.info_index ? a.info_index[s] : s;
         atomicCAS(&a.info[fi].status, CHP_SYS_OK, CHP_SYS_NONFINITE);
       }
@@ -216,10 +237,24 @@ struct ColArgs {
   double* buf;
   long long stride;
   int m;
-  double a2dt, b, scale;   // den = (1 - a2dt*lam) + b*lam^2 ; scale = (2/N)^2
-  const double* lam;       // lam[p], p = 1..m (index 0 unused)
+  const double* dtab;      // D'[q][p] = (2/N)^2 / ((1 - 2dt lam) + b lam^2), lam = lam_p + lam_q
   const double2* wtab;
 };
+
+// D' table for one (N, dt, eps): [q][p], zero on the pad row / column.  Exact
+// division (the column pass only multiplies).
+__global__ void k2d_build_dtab(int N, const double* lam, double a2dt, double b, double scale,
+                               double* d) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)N * N) return;
+  const int q = (int)(t / N), p = (int)(t % N);
+  double v = 0.0;
+  if (p > 0 && q > 0) {
+    const double l = lam[p] + lam[q];
+    v = scale / ((1.0 - a2dt * l) + b * (l * l));
+  }
+  d[t] = v;
+}
 
 template <int N>
 CHP_DEV int csw(int c, int n) { return c * N + (n ^ c ^ (((n >> 5) & 15) << 1)); }
@@ -261,18 +296,17 @@ k2d_col_pass_b(ColArgs a) {
     y = z ? 0.0 : sm[csw<N>(cb, n)];
     ym = z ? 0.0 : sm[csw<N>(cb, N - n)];
   };
-  auto dscale = [&](int p, int q) -> double {
-    if (p == 0 || q == 0) return 0.0;
-    const double lam = a.lam[p] + a.lam[q];
-    return a.scale * wdst::rcp((1.0 - a.a2dt * lam) + a.b * (lam * lam));
-  };
+  const double* __restrict__ da = a.dtab + (long long)(grp ? qa : 0) * N;
+  const double* __restrict__ db = a.dtab + (long long)(grp ? qb : 0) * N;
   auto st = [&](int k, double a2, double a21, double b2, double b21) {
     if (!grp) return;
     if (scale_pass) {
-      a2 *= dscale(2 * k, qa);
-      a21 *= dscale(2 * k + 1, qa);
-      b2 *= dscale(2 * k, qb);
-      b21 *= dscale(2 * k + 1, qb);
+      const double2 sa = __ldg(reinterpret_cast<const double2*>(da + 2 * k));
+      const double2 sb = __ldg(reinterpret_cast<const double2*>(db + 2 * k));
+      a2 *= sa.x;
+      a21 *= sa.y;
+      b2 *= sb.x;
+      b21 *= sb.y;
     }
     sm[csw<N>(ca, 2 * k)] = a2;
     sm[csw<N>(ca, 2 * k + 1)] = a21;
@@ -866,18 +900,15 @@ CHP_DEV void coop_total(const double* part, double* red, double (&out)[K]) {
 // row-pair DST over the field: dst rows = T_j src rows (+ optional CG op)
 //   op 0: dst = T_j src
 //   op 1: dst = d .* p + T_j src ; returns thread partial of p.q
-//   op 2: CG direction update fused in: src = P is replaced by
-//         P = R / M + beta P (M = d + acbar) before the transform
 template <int N>
-CHP_DEV double coop_zinv(const CoopArgs& a, int r, int n, double acbar) {
+CHP_DEV double coop_precond(const CoopArgs& a, int r, int n, double acbar) {   // M(r, n)
   const double kap = -(a.lam[r + 1] + a.lam[n]);
-  return wdst::rcp((wdst::rcp(kap) + a.b * kap) + acbar);
+  return (1.0 / kap + a.b * kap) + acbar;
 }
 
 template <int N>
 __device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, double* dst, int op,
-                                         const double* p, double beta = 0.0, double acbar = 0.0,
-                                         double* dst2 = nullptr, const double* Rv = nullptr) {
+                                         const double* p) {
   const auto& a = x.a;
   const int m = a.m;
   double part = 0.0;
@@ -894,23 +925,6 @@ __device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, doubl
     const double* sb = src + (long long)(vb ? rb : ra) * N;
     auto ld = [&](int n, double& u, double& um, double& v, double& vm) {
       const bool z = n == 0 || !have;
-      if (op == 2) {
-        // p = r/M + beta p at (ra, n), (ra, N-n), (rb, n), (rb, N-n); the
-        // primary index n writes P back (each point has exactly one primary)
-        const long long oa = (long long)ra * N, ob = (long long)rb * N;
-        auto pn = [&](long long o, int r, int nn) {
-          return fma(beta, src[o + nn], Rv[o + nn] * coop_zinv<N>(a, r, nn, acbar));
-        };
-        u = z ? 0.0 : pn(oa, ra, n);
-        um = z ? 0.0 : pn(oa, ra, N - n);
-        v = (z || !vb) ? 0.0 : pn(ob, rb, n);
-        vm = (z || !vb) ? 0.0 : pn(ob, rb, N - n);
-        if (!z) {                     // new direction into the other P buffer
-          dst2[oa + n] = u;
-          if (vb) dst2[ob + n] = v;
-        }
-        return;
-      }
       u = z ? 0.0 : sa[n];
       um = z ? 0.0 : sa[N - n];
       v = (z || !vb) ? 0.0 : sb[n];
@@ -1111,7 +1125,7 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
           double z = 0.0;
           if (j > 0) {
             const double rv = Rv[t];
-            z = rv * coop_zinv<N>(a, i, j, acbar);
+            z = rv / coop_precond<N>(a, i, j, acbar);
             pr[0] = fma(rv, z, pr[0]);
             pr[1] = fma(rv, rv, pr[1]);
           }
@@ -1127,21 +1141,13 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
         int it = 0;
         bool fail = false;
         bool done = !(rr0 > 0.0);
-        double beta = 0.0;
-        double* Pc = Pv;                     // current direction; Cv is free after CT
-        double* Pn = Cv;
         while (!done) {
-          if (it == 0) {
-            coop_rows<N>(x, Pc, Yv, 0, nullptr);
-          } else {
-            coop_rows<N>(x, Pc, Yv, 2, nullptr, beta, acbar, Pn, Rv);
-            double* t = Pc; Pc = Pn; Pn = t;
-          }
+          coop_rows<N>(x, Pv, Yv, 0, nullptr);
           gbar(grid);
           coop_cols<N>(x, Yv, Yv, 1, a.dt * s2, CT);
           gbar(grid);
           double pq[1];
-          pq[0] = coop_rows<N>(x, Yv, Yv, 1, Pc);
+          pq[0] = coop_rows<N>(x, Yv, Yv, 1, Pv);
           pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
           coop_block_partials<1>(pq, red, pbuf);
           gbar(grid);
@@ -1152,10 +1158,10 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
           for (long long t = gtid; t < tot; t += gstride) {
             const int i = (int)(t / N), j = (int)(t % N);
             if (j == 0) continue;
-            X[t] = fma(alpha, Pc[t], X[t]);
+            X[t] = fma(alpha, Pv[t], X[t]);
             const double rv = fma(-alpha, Yv[t], Rv[t]);
             Rv[t] = rv;
-            rz[0] = fma(rv, rv * coop_zinv<N>(a, i, j, acbar), rz[0]);
+            rz[0] = fma(rv, rv / coop_precond<N>(a, i, j, acbar), rz[0]);
             rz[1] = fma(rv, rv, rz[1]);
           }
           pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
@@ -1163,13 +1169,19 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
           gbar(grid);
           double t1[2];
           coop_total<2>(pbuf, red, t1);
-          beta = t1[0] / rho;
+          const double beta = t1[0] / rho;
           rho = t1[0];
           ++it;
           if (!(t1[1] > tol2 * rr0)) done = true;
           else if (it >= a.max_iter) { done = true; fail = true; }
           if (!isfinite(t1[1])) { done = true; fail = true; }
           if (done) break;
+          for (long long t = gtid; t < tot; t += gstride) {
+            const int i = (int)(t / N), j = (int)(t % N);
+            if (j == 0) continue;
+            Pv[t] = fma(beta, Pv[t], Rv[t] / coop_precond<N>(a, i, j, acbar));
+          }
+          gbar(grid);
         }
         if (gtid == 0) {
           a.info[ic].cg_total += it;
@@ -1256,7 +1268,7 @@ template <int N>
 cudaError_t run_linear_b(const chp_grid& g, const chp_spec& sp, int steps, int nsys,
                          const double* in, long long in_stride, double* out, long long out_stride,
                          const int* sys_index, chp_sys_info* info, const NTables& nt,
-                         double* scratch, cudaStream_t st) {
+                         double* scratch, const double* dtab, cudaStream_t st) {
   using C = WCfg<N>;
   set_smem_attrs<N>();
   const int m = g.m;
@@ -1264,7 +1276,7 @@ cudaError_t run_linear_b(const chp_grid& g, const chp_spec& sp, int steps, int n
   double* buf[2] = {scratch, scratch + fs * nsys};
   using CC = WCfgC<N>;
   const dim3 rgrid((m + C::TR - 1) / C::TR, nsys), cgrid(N / CC::TC, nsys);
-  ColArgs ca{nullptr, fs, m, 2.0 * sp.dt, sp.b, (2.0 / N) * (2.0 / N), nt.lam, nt.wtab};
+  ColArgs ca{nullptr, fs, m, dtab, nt.wtab};
   for (int s = 0; s < steps; ++s) {
     RowArgs ra{};
     ra.m = m; ra.dt = sp.dt; ra.c1 = g.c1; ra.info = info; ra.info_index = sys_index;
@@ -1387,6 +1399,8 @@ struct Chp2d {
   double* host_res = nullptr;     // pinned
   NewtonRec* host_rec = nullptr;  // pinned
   int host_cap = 0;
+  struct DTab { int N; double a2dt, b; double* d; };
+  std::vector<DTab> dtabs;        // LINEAR_B spectral divisors, one per (N, dt, eps)
 };
 
 Chp2d* chp2d_create() { return new Chp2d(); }
@@ -1400,6 +1414,7 @@ void chp2d_destroy(Chp2d* c) {
     cudaFree(kv.second.wtab);
   }
   if (c->scratch) cudaFree(c->scratch);
+  for (auto& t : c->dtabs) cudaFree(t.d);
   if (c->work) cudaFree(c->work);
   if (c->host_act) cudaFreeHost(c->host_act);
   if (c->host_res) cudaFreeHost(c->host_res);
@@ -1608,6 +1623,28 @@ bool pow2_ok(const chp_grid& g, std::string* err) {
   return true;
 }
 
+cudaError_t get_dtab(Chp2d* c, int N, const chp_spec& sp, const NTables& nt, const double** out,
+                     cudaStream_t st) {
+  const double a2dt = 2.0 * sp.dt, b = sp.b;
+  for (auto& t : c->dtabs)
+    if (t.N == N && t.a2dt == a2dt && t.b == b) { *out = t.d; return cudaSuccess; }
+  if (c->dtabs.size() >= 8) {              // bounded cache: drop the oldest table
+    cudaStreamSynchronize(st);
+    cudaFree(c->dtabs.front().d);
+    c->dtabs.erase(c->dtabs.begin());
+  }
+  Chp2d::DTab t{N, a2dt, b, nullptr};
+  cudaError_t e = cudaMalloc(&t.d, sizeof(double) * (size_t)N * N);
+  if (e != cudaSuccess) return e;
+  const long long n = (long long)N * N;
+  k2d_build_dtab<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(N, nt.lam, a2dt, b,
+                                                            (2.0 / N) * (2.0 / N), t.d);
+  c->dtabs.push_back(t);
+  *out = t.d;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cudaStreamSynchronize(st);        // usable from any stream afterwards
+}
+
 template <int N>
 cudaError_t propagate_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int steps, int nsys,
                         const double* in, long long in_stride, double* out, long long out_stride,
@@ -1617,8 +1654,10 @@ cudaError_t propagate_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int ste
     cudaError_t e = grow(reinterpret_cast<void**>(&c->scratch), &c->scratch_bytes,
                          2 * fs * nsys * sizeof(double), st);
     if (e != cudaSuccess) return e;
+    const double* dtab = nullptr;
+    if ((e = get_dtab(c, N, sp, nt, &dtab, st)) != cudaSuccess) return e;
     return run_linear_b<N>(g, sp, steps, nsys, in, in_stride, out, out_stride, idx, info, nt,
-                           c->scratch, st);
+                           c->scratch, dtab, st);
   }
   Work2 W;
   cudaError_t e = get_work(c, fs, nsys, &W, st);
