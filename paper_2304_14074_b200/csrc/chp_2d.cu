@@ -154,46 +154,54 @@ k2d_row_pass(RowArgs a) {
     } else {
       oa = active && ra < m;
       ob = active && rb < m;
-      // rhs = x + dt L w, w = x^3 - 3x: centre x into registers, then w in
-      // place over the whole tile (one cube per point), the 5-point stencil
-      // of w, and finally the rhs into this group's rows
+      // rhs = x + dt L w, w = x^3 - 3x, for the lane's contiguous chunk of
+      // PL points of rows r0 and r0+1: pairs (n, n+1) read as double2 from the
+      // tile (conflict free under rsw), w computed once per value read, the
+      // horizontal neighbours carried in registers.  Stencil order as the
+      // reference's CSR matvec: (i-1,j), (i,j-1), (i,j), (i,j+1), (i+1,j).
       double la[PL], lb[PL];
       const int r0 = 1 + 2 * g;
-#pragma unroll
-      for (int i = 0; i < PL; ++i) {
-        const int n = l + L * i;
-        la[i] = active ? sm[(size_t)r0 * N + wdst::rsw(n)] : 0.0;
-        lb[i] = active ? sm[(size_t)(r0 + 1) * N + wdst::rsw(n)] : 0.0;
-      }
-      __syncthreads();
-      for (int idx = tid; idx < C::ROWS * N / 2; idx += C::THREADS) {
-        double2* p2 = reinterpret_cast<double2*>(sm) + idx;   // rsw keeps (2k, 2k+1) pairs
-        const double2 v = *p2;
-        *p2 = make_double2(w_of(v.x), w_of(v.y));
-      }
-      __syncthreads();
-      auto wat = [&](int r, int n) -> double { return sm[(size_t)r * N + wdst::rsw(n)]; };
-      auto lw = [&](int r, int n) -> double {
-        const double wr = (n + 1 < N) ? wat(r, n + 1) : 0.0;
-        return (((wat(r - 1, n) * c + wat(r, n - 1) * c) + wat(r, n) * c4) + wr * c) +
-               wat(r + 1, n) * c;
+      const int nb = l * PL;
+      auto ld2 = [&](int r, int n) -> double2 {
+        return *reinterpret_cast<const double2*>(sm + (size_t)r * N + wdst::rsw(n));
       };
-#pragma unroll
-      for (int i = 0; i < PL; ++i) {
-        const int n = l + L * i;
-        if (active && n > 0) {
-          la[i] = la[i] + dt * lw(r0, n);
-          lb[i] = lb[i] + dt * lw(r0 + 1, n);
-        } else {
-          la[i] = 0.0;
-          lb[i] = 0.0;
+      auto w2 = [](double2 v) { return make_double2(w_of(v.x), w_of(v.y)); };
+      if (active) {
+        double wam = 0.0, wbm = 0.0;                 // w at n - 1
+        if (nb > 0) {
+          wam = w_of(sm[(size_t)r0 * N + wdst::rsw(nb - 1)]);
+          wbm = w_of(sm[(size_t)(r0 + 1) * N + wdst::rsw(nb - 1)]);
         }
+        double2 xa = ld2(r0, nb), xb = ld2(r0 + 1, nb);
+        double2 wa = w2(xa), wb = w2(xb);
+#pragma unroll
+        for (int j = 0; j < PL / 2; ++j) {
+          const int n = nb + 2 * j;
+          const bool more = n + 2 < N;
+          const double2 xan = more ? ld2(r0, n + 2) : make_double2(0.0, 0.0);
+          const double2 xbn = more ? ld2(r0 + 1, n + 2) : make_double2(0.0, 0.0);
+          const double2 wup = w2(ld2(r0 - 1, n)), wdn = w2(ld2(r0 + 2, n));
+          const double2 wan = w2(xan), wbn = w2(xbn);
+          const double la0 = (((wup.x * c + wam * c) + wa.x * c4) + wa.y * c) + wb.x * c;
+          const double la1 = (((wup.y * c + wa.x * c) + wa.y * c4) + wan.x * c) + wb.y * c;
+          const double lb0 = (((wa.x * c + wbm * c) + wb.x * c4) + wb.y * c) + wdn.x * c;
+          const double lb1 = (((wa.y * c + wb.x * c) + wb.y * c4) + wbn.x * c) + wdn.y * c;
+          la[2 * j] = (n > 0) ? xa.x + dt * la0 : 0.0;
+          lb[2 * j] = (n > 0) ? xb.x + dt * lb0 : 0.0;
+          la[2 * j + 1] = xa.y + dt * la1;
+          lb[2 * j + 1] = xb.y + dt * lb1;
+          wam = wa.y; wbm = wb.y;
+          xa = xan; xb = xbn; wa = wan; wb = wbn;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < PL; ++i) { la[i] = 0.0; lb[i] = 0.0; }
       }
       __syncthreads();
 #pragma unroll
-      for (int i = 0; i < PL; ++i) {
-        wr0[wdst::rsw(l + L * i)] = la[i];
-        wr1[wdst::rsw(l + L * i)] = lb[i];
+      for (int j = 0; j < PL / 2; ++j) {
+        *reinterpret_cast<double2*>(wr0 + wdst::rsw(nb + 2 * j)) = make_double2(la[2 * j], la[2 * j + 1]);
+        *reinterpret_cast<double2*>(wr1 + wdst::rsw(nb + 2 * j)) = make_double2(lb[2 * j], lb[2 * j + 1]);
       }
       wdst::group_sync<N>();
     }
