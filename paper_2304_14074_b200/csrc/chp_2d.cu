@@ -822,6 +822,8 @@ struct CoopArgs {
   double* U; const double* F; double* G; long long ics, sls;
   unsigned char* changed; double* inc; chp_sys_info* info;
   double *X, *Rv, *Pv, *Yv, *Cv, *CT;   // per-IC work fields (stride fs), nic-major
+  double* Mi;                            // 1 / preconditioner (per IC, stride fs)
+  double* Dk;                            // 1/kappa + b kappa ([m][N], shared by all ICs)
   double* part;                          // [2][gridDim][8] block partials
   unsigned int* bar;                     // grid barrier counter (zeroed by the host)
   const double* lam; const double2* wtab;
@@ -858,10 +860,22 @@ CHP_DEV void gbar(GridBar& b) {
   __syncthreads();
 }
 
+// lanes per pair in the cooperative coarse kernel: one pair per two warps at
+// N = 1024 (a single field leaves most of the GPU idle with one warp per pair)
+template <int N> struct CoopGeo {
+  static constexpr int L = (N == 1024) ? 64 : wdst::Geo<N>::L;
+  static constexpr int GPB = 256 / L;
+  // op-1 operands (p rows, d rows) staged in shared memory when they fit
+  static constexpr bool STAGE_P = (size_t)GPB * 6 * N * 8 + 16 * (size_t)(N + 64) <= 200 * 1024;
+  static constexpr size_t SMEM =
+      sizeof(double) * (size_t)GPB * (STAGE_P ? 6 : 2) * N + 16 * (size_t)(N + 64);
+};
+
 template <int N>
 struct CoopCtx {
   const CoopArgs& a;
-  double* sm;          // dynamic smem: GPB groups x 2N doubles, then twiddles (N double2)
+  double* sm;          // dynamic smem: GPB groups x 2N doubles (row pairs / column tile),
+  double* sm2;         // [STAGE_P] GPB groups x 4N doubles (op-1 operands), then twiddles
   double2* twt;
   double* red;         // 32 doubles of static smem for block reductions
   int tid, g, l, gpb, ngroups, gg;
@@ -908,19 +922,23 @@ CHP_DEV void coop_total(const double* part, double* red, double (&out)[K]) {
 // row-pair DST over the field: dst rows = T_j src rows (+ optional CG op)
 //   op 0: dst = T_j src
 //   op 1: dst = d .* p + T_j src ; returns thread partial of p.q
-template <int N>
-CHP_DEV double coop_precond(const CoopArgs& a, int r, int n, double acbar) {   // M(r, n)
-  const double kap = -(a.lam[r + 1] + a.lam[n]);
-  return (1.0 / kap + a.b * kap) + acbar;
-}
-
+// With upd != nullptr the group first applies the CG direction update to its
+// two rows in place, src = upd: P = R / M + beta P (no separate grid phase).
 template <int N>
 __device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, double* dst, int op,
-                                         const double* p) {
+                                         const double* p, double* upd = nullptr,
+                                         const double* Rv = nullptr, double beta = 0.0,
+                                         const double* Mi = nullptr) {
+  constexpr int L = CoopGeo<N>::L;
   const auto& a = x.a;
   const int m = a.m;
   double part = 0.0;
-  double2* scr = reinterpret_cast<double2*>(x.sm + (size_t)x.g * 2 * N);
+  // the group's two source rows are staged in its scratch (cp.async, all in
+  // flight at once) and consumed by in() before the FFT reuses the space
+  double* rows = x.sm + (size_t)x.g * 2 * N;
+  double2* scr = reinterpret_cast<double2*>(rows);
+  // op 1: p rows and d rows (1/kappa + b kappa) staged in the second region
+  double* prow = CoopGeo<N>::STAGE_P ? x.sm2 + (size_t)x.g * 4 * N : nullptr;
   // whole warps iterate together (pair_dst needs every lane of the warp);
   // groups without a pair run on zeros and store nothing
   for (int it = 0;; ++it) {
@@ -929,29 +947,63 @@ __device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, doubl
     if (!__any_sync(0xffffffffu, have)) break;
     const int ra = have ? 2 * pr : 0, rb = ra + 1;
     const bool vb = have && rb < m;
-    const double* sa = src + (long long)ra * N;
-    const double* sb = src + (long long)(vb ? rb : ra) * N;
+    if (have) {
+      const int nr = vb ? 2 : 1;
+      if (upd) {
+        // CG direction update of the two rows: P = R / M + beta P
+        for (int h = 0; h < nr; ++h) {
+          const long long o = (long long)(ra + h) * N;
+          for (int n = x.l; n < N; n += L) {
+            double v = 0.0;
+            if (n > 0) {
+              v = fma(beta, upd[o + n], Rv[o + n] * Mi[o + n]);
+              upd[o + n] = v;
+            }
+            rows[h * N + n] = v;
+          }
+        }
+      } else {
+        for (int idx = x.l; idx < nr * (N / 2); idx += L) {
+          const int h = idx / (N / 2), jj = 2 * (idx % (N / 2));
+          cp_async16(rows + h * N + jj, src + (long long)(ra + h) * N + jj);
+        }
+      }
+      if (op == 1 && prow) {
+        for (int idx = x.l; idx < nr * (N / 2); idx += L) {
+          const int h = idx / (N / 2), jj = 2 * (idx % (N / 2));
+          cp_async16(prow + h * N + jj, p + (long long)(ra + h) * N + jj);
+          cp_async16(prow + 2 * N + h * N + jj, a.Dk + (long long)(ra + h) * N + jj);
+        }
+      }
+      cp_async_wait_all();
+    }
+    wdst::group_sync<N, L>();
     auto ld = [&](int n, double& u, double& um, double& v, double& vm) {
       const bool z = n == 0 || !have;
-      u = z ? 0.0 : sa[n];
-      um = z ? 0.0 : sa[N - n];
-      v = (z || !vb) ? 0.0 : sb[n];
-      vm = (z || !vb) ? 0.0 : sb[N - n];
+      u = z ? 0.0 : rows[n];
+      um = z ? 0.0 : rows[N - n];
+      v = (z || !vb) ? 0.0 : rows[N + n];
+      vm = (z || !vb) ? 0.0 : rows[2 * N - n];
     };
     auto st = [&](int k, double a2, double a21, double b2, double b21) {
       if (!have) return;
       if (op == 1) {
-        const int r0 = ra;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int r = r0 + h;
+          const int r = ra + h;
           if (r >= m) break;
           double y0 = h ? b2 : a2, y1 = h ? b21 : a21;
-          const double2 pv = *reinterpret_cast<const double2*>(p + (long long)r * N + 2 * k);
-          const double k0 = -(a.lam[r + 1] + a.lam[2 * k]), k1 = -(a.lam[r + 1] + a.lam[2 * k + 1]);
-          if (k > 0) { y0 = fma(1.0 / k0 + a.b * k0, pv.x, y0); part = fma(pv.x, y0, part); }
+          double2 pv, dv;
+          if (prow) {
+            pv = *reinterpret_cast<const double2*>(prow + h * N + 2 * k);
+            dv = *reinterpret_cast<const double2*>(prow + 2 * N + h * N + 2 * k);
+          } else {
+            pv = *reinterpret_cast<const double2*>(p + (long long)r * N + 2 * k);
+            dv = *reinterpret_cast<const double2*>(a.Dk + (long long)r * N + 2 * k);
+          }
+          if (k > 0) { y0 = fma(dv.x, pv.x, y0); part = fma(pv.x, y0, part); }
           else y0 = 0.0;
-          y1 = fma(1.0 / k1 + a.b * k1, pv.y, y1);
+          y1 = fma(dv.y, pv.y, y1);
           part = fma(pv.y, y1, part);
           *reinterpret_cast<double2*>(dst + (long long)r * N + 2 * k) = make_double2(y0, y1);
         }
@@ -960,8 +1012,8 @@ __device__ __noinline__ double coop_rows(CoopCtx<N>& x, const double* src, doubl
         if (vb) *reinterpret_cast<double2*>(dst + (long long)rb * N + 2 * k) = make_double2(b2, b21);
       }
     };
-    wdst::pair_dst<N>(ld, st, scr, x.twt, x.l, x.ac);
-    wdst::group_sync<N>();
+    wdst::pair_dst<N, L>(ld, st, scr, x.twt, x.l, x.ac);
+    wdst::group_sync<N, L>();
   }
   return part;
 }
@@ -985,14 +1037,25 @@ __device__ __noinline__ void coop_cols(CoopCtx<N>& x, const double* src, double*
   double2* scr = reinterpret_cast<double2*>(x.sm + (size_t)ca * N);
   for (int tile = blockIdx.x; tile < N / TC; tile += gridDim.x) {
     const int j0 = tile * TC;
-#pragma unroll 8
     for (int idx = threadIdx.x; idx < N * TC; idx += blockDim.x) {
       const int n = idx / TC, cc = idx % TC;
-      x.sm[csw<N>(cc, n)] = (n > 0 && j0 + cc > 0) ? src[(long long)(n - 1) * N + j0 + cc] : 0.0;
+      if (n > 0 && j0 + cc > 0) cp_async8(&x.sm[csw<N>(cc, n)], src + (long long)(n - 1) * N + j0 + cc);
+      else x.sm[csw<N>(cc, n)] = 0.0;
     }
-    __syncthreads();
     const int qa = j0 + ca, qb = j0 + cb;
     const bool act = ca < TC;
+    // op 1: this group's two rows of c^T staged next to the tile
+    double* crow = (CoopGeo<N>::STAGE_P && op == 1) ? x.sm2 + (size_t)x.g * 4 * N : nullptr;
+    if (crow && act) {
+      const double* ga = cT + (long long)(qa > 0 ? qa - 1 : 0) * N;
+      const double* gb = cT + (long long)(qb - 1) * N;
+      for (int jj = 2 * x.l; jj < N; jj += 2 * CoopGeo<N>::L) {
+        cp_async16(crow + jj, ga + jj);
+        cp_async16(crow + N + jj, gb + jj);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
     auto ld = [&](int n, double& u, double& um, double& v, double& vm) {
       const bool z = n == 0 || !act;
       u = z ? 0.0 : x.sm[csw<N>(ca, n)];
@@ -1006,8 +1069,10 @@ __device__ __noinline__ void coop_cols(CoopCtx<N>& x, const double* src, double*
       const int p0 = 2 * k, p1 = p0 + 1;
       if (op == 1 && pass == 0) {
         // column qa = 0 is the pad (its outputs are zeroed below)
-        const double2 c_a = *reinterpret_cast<const double2*>(cT + (long long)(qa > 0 ? qa - 1 : 0) * N + p0);
-        const double2 c_b = *reinterpret_cast<const double2*>(cT + (long long)(qb - 1) * N + p0);
+        const double2 c_a = crow ? *reinterpret_cast<const double2*>(crow + p0)
+                                 : *reinterpret_cast<const double2*>(cT + (long long)(qa > 0 ? qa - 1 : 0) * N + p0);
+        const double2 c_b = crow ? *reinterpret_cast<const double2*>(crow + N + p0)
+                                 : *reinterpret_cast<const double2*>(cT + (long long)(qb - 1) * N + p0);
         a2 *= scale * c_a.x; a21 *= scale * c_a.y;
         b2 *= scale * c_b.x; b21 *= scale * c_b.y;
       } else if (op == 0) {
@@ -1025,12 +1090,12 @@ __device__ __noinline__ void coop_cols(CoopCtx<N>& x, const double* src, double*
     };
     // every group runs (small N: several groups share a warp); groups beyond
     // the tile read zeros and store nothing
-    wdst::pair_dst<N>(ld, st, scr, x.twt, x.l, x.ac);
-    wdst::group_sync<N>();
+    wdst::pair_dst<N, CoopGeo<N>::L>(ld, st, scr, x.twt, x.l, x.ac);
+    wdst::group_sync<N, CoopGeo<N>::L>();
     if (op == 1) {
       pass = 1;
-      wdst::pair_dst<N>(ld, st, scr, x.twt, x.l, x.ac);
-      wdst::group_sync<N>();
+      wdst::pair_dst<N, CoopGeo<N>::L>(ld, st, scr, x.twt, x.l, x.ac);
+      wdst::group_sync<N, CoopGeo<N>::L>();
     }
     __syncthreads();
 #pragma unroll 8
@@ -1048,11 +1113,12 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
   GridBar grid{a.bar, 0u, a.trace, a.trace_cap};
   extern __shared__ __align__(16) double smc[];
   __shared__ double red[64];
-  constexpr int L = wdst::Geo<N>::L;
+  constexpr int L = CoopGeo<N>::L;
   CoopCtx<N> x{a};
   x.sm = smc;
   x.gpb = blockDim.x / L;
-  x.twt = reinterpret_cast<double2*>(smc + (size_t)x.gpb * 2 * N);
+  x.sm2 = smc + (size_t)x.gpb * 2 * N;
+  x.twt = reinterpret_cast<double2*>(smc + (size_t)x.gpb * (CoopGeo<N>::STAGE_P ? 6 : 2) * N);
   x.red = red;
   x.tid = threadIdx.x;
   x.g = x.tid / L;
@@ -1069,6 +1135,17 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
   const long long gstride = (long long)gridDim.x * blockDim.x;
   const double s2 = (2.0 / N) * (2.0 / N);
   const double tol2 = a.tol * a.tol;
+  // d = 1/kappa + b kappa (the constant part of the operator and of M); visible
+  // to all blocks after the first slice barrier
+  for (long long t = gtid; t < tot; t += gstride) {
+    const int i = (int)(t / N), j = (int)(t % N);
+    double d = 0.0;
+    if (j > 0) {
+      const double kap = -(a.lam[i + 1] + a.lam[j]);
+      d = 1.0 / kap + a.b * kap;
+    }
+    a.Dk[t] = d;
+  }
   int pb = 0;                                      // alternating partial buffer
 
   for (int ic = 0; ic < a.nic; ++ic) {
@@ -1077,6 +1154,7 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
     double* Pv = a.Pv + ic * fs;
     double* Yv = a.Yv + ic * fs;
     double* Cv = a.Cv + ic * fs;
+    double* Mi = a.Mi + ic * fs;
     double* CT = a.CT + ic * fs;
     unsigned char* ch = a.changed ? a.changed + (long long)ic * (a.nsl + 1) : nullptr;
     double* Ui = a.U + ic * a.ics;
@@ -1115,10 +1193,12 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
         double tc[1];
         coop_total<1>(pbuf, red, tc);
         const double acbar = a.dt * (tc[0] / ((double)m * m));
-        // c transposed for the column phases: CT[q-1][n] = c[n-1][q], q, n = 1..m
+        // c transposed for the column phases: CT[q-1][n] = c[n-1][q], q, n = 1..m;
+        // the inverse preconditioner 1 / M, M = 1/kappa + b kappa + dt mean(c)
         for (long long t = gtid; t < tot; t += gstride) {
           const int q1 = (int)(t / N), nn = (int)(t % N);
           CT[t] = (nn > 0) ? Cv[(long long)(nn - 1) * N + q1 + 1] : 0.0;
+          Mi[t] = (nn > 0) ? 1.0 / (a.Dk[t] + acbar) : 0.0;
         }
         // ---- b^ = (2/N)/kappa .* T_i T_j rhs -> Rv -----------------------------
         coop_rows<N>(x, Yv, Yv, 0, nullptr);
@@ -1133,7 +1213,7 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
           double z = 0.0;
           if (j > 0) {
             const double rv = Rv[t];
-            z = rv / coop_precond<N>(a, i, j, acbar);
+            z = rv * Mi[t];
             pr[0] = fma(rv, z, pr[0]);
             pr[1] = fma(rv, rv, pr[1]);
           }
@@ -1149,8 +1229,10 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
         int it = 0;
         bool fail = false;
         bool done = !(rr0 > 0.0);
+        double beta = 0.0;
         while (!done) {
-          coop_rows<N>(x, Pv, Yv, 0, nullptr);
+          if (it == 0) coop_rows<N>(x, Pv, Yv, 0, nullptr);
+          else coop_rows<N>(x, Pv, Yv, 0, nullptr, Pv, Rv, beta, Mi);
           gbar(grid);
           coop_cols<N>(x, Yv, Yv, 1, a.dt * s2, CT);
           gbar(grid);
@@ -1162,34 +1244,42 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
           double tq[1];
           coop_total<1>(pbuf, red, tq);
           const double alpha = rho / tq[0];
+          // X += alpha P, R -= alpha Q; (r.z, r.r).  Pad entries are zero in
+          // every field (and Mi), so the loop runs over whole rows as double2.
           double rz[2] = {0.0, 0.0};
-          for (long long t = gtid; t < tot; t += gstride) {
-            const int i = (int)(t / N), j = (int)(t % N);
-            if (j == 0) continue;
-            X[t] = fma(alpha, Pv[t], X[t]);
-            const double rv = fma(-alpha, Yv[t], Rv[t]);
-            Rv[t] = rv;
-            rz[0] = fma(rv, rv / coop_precond<N>(a, i, j, acbar), rz[0]);
-            rz[1] = fma(rv, rv, rz[1]);
+          {
+            double2* X2 = reinterpret_cast<double2*>(X);
+            double2* R2 = reinterpret_cast<double2*>(Rv);
+            const double2* P2 = reinterpret_cast<const double2*>(Pv);
+            const double2* Y2 = reinterpret_cast<const double2*>(Yv);
+            const double2* M2 = reinterpret_cast<const double2*>(Mi);
+#pragma unroll 4
+            for (long long t = gtid; t < tot / 2; t += gstride) {
+              double2 xv = X2[t], rv = R2[t];
+              const double2 pv = P2[t], yv = Y2[t], mi = M2[t];
+              xv.x = fma(alpha, pv.x, xv.x);
+              xv.y = fma(alpha, pv.y, xv.y);
+              rv.x = fma(-alpha, yv.x, rv.x);
+              rv.y = fma(-alpha, yv.y, rv.y);
+              X2[t] = xv;
+              R2[t] = rv;
+              rz[0] = fma(rv.x, rv.x * mi.x, rz[0]);
+              rz[0] = fma(rv.y, rv.y * mi.y, rz[0]);
+              rz[1] = fma(rv.x, rv.x, rz[1]);
+              rz[1] = fma(rv.y, rv.y, rz[1]);
+            }
           }
           pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
           coop_block_partials<2>(rz, red, pbuf);
           gbar(grid);
           double t1[2];
           coop_total<2>(pbuf, red, t1);
-          const double beta = t1[0] / rho;
+          beta = t1[0] / rho;
           rho = t1[0];
           ++it;
           if (!(t1[1] > tol2 * rr0)) done = true;
           else if (it >= a.max_iter) { done = true; fail = true; }
           if (!isfinite(t1[1])) { done = true; fail = true; }
-          if (done) break;
-          for (long long t = gtid; t < tot; t += gstride) {
-            const int i = (int)(t / N), j = (int)(t % N);
-            if (j == 0) continue;
-            Pv[t] = fma(beta, Pv[t], Rv[t] / coop_precond<N>(a, i, j, acbar));
-          }
-          gbar(grid);
         }
         if (gtid == 0) {
           a.info[ic].cg_total += it;
@@ -1245,6 +1335,7 @@ struct NTables {
   double* sj = nullptr;
   double* lam = nullptr;   // per-axis eigenvalues, index p = 1..m
   double2* wtab = nullptr; // wdst lane tables: (cos, sin)(pi l/N), then W_N^l
+  double2* wtab_coop = nullptr;  // the same for the coarse kernel's 64-lane geometry (N = 1024)
 };
 
 struct Work2 {            // device workspace for one solve batch
@@ -1420,6 +1511,7 @@ void chp2d_destroy(Chp2d* c) {
     cudaFree(kv.second.sj);
     cudaFree(kv.second.lam);
     cudaFree(kv.second.wtab);
+    if (kv.second.wtab_coop) cudaFree(kv.second.wtab_coop);
   }
   if (c->scratch) cudaFree(c->scratch);
   for (auto& t : c->dtabs) cudaFree(t.d);
@@ -1449,24 +1541,33 @@ cudaError_t get_tables(Chp2d* c, int N, const NTables** out) {
     const long double sp = sinl(pi * p / (2.0L * N));
     lam[p] = (double)(-4.0L / (h * h) * sp * sp);
   }
-  std::vector<double2> wt(2 * N + 64);
-  // lanes of the wdst geometry for N (wdst::Geo)
-  const int wl = N == 8 ? 2 : N <= 32 ? 4 : N <= 128 ? 8 : N <= 512 ? 16 : wdst::Geo<1024>::L;
-  for (int k = 0; k < 64; ++k) {
-    const long double ang = 2.0L * pi * k / 64;
-    wt[2 * N + k] = make_double2((double)cosl(ang), (double)-sinl(ang));
-  }
-  for (int l = 0; l < N; ++l)
-    wt[l] = make_double2((double)cosl(pi * l / N), (double)sinl(pi * l / N));
-  for (int k2 = 0; k2 < N / wl; ++k2)
-    for (int l = 0; l < wl; ++l) {
-      const long double ang = 2.0L * pi * (long double)((l * k2) % N) / N;
-      wt[N + k2 * wl + l] = make_double2((double)cosl(ang), (double)-sinl(ang));
+  // lane tables of a wdst geometry with wl lanes per group
+  auto lane_tables = [&](int wl) {
+    std::vector<double2> wt(2 * N + 64);
+    for (int k = 0; k < 64; ++k) {
+      const long double ang = 2.0L * pi * k / 64;
+      wt[2 * N + k] = make_double2((double)cosl(ang), (double)-sinl(ang));
     }
+    for (int l = 0; l < N; ++l)
+      wt[l] = make_double2((double)cosl(pi * l / N), (double)sinl(pi * l / N));
+    for (int k2 = 0; k2 < N / wl; ++k2)
+      for (int l = 0; l < wl; ++l) {
+        const long double ang = 2.0L * pi * (long double)((l * k2) % N) / N;
+        wt[N + k2 * wl + l] = make_double2((double)cosl(ang), (double)-sinl(ang));
+      }
+    return wt;
+  };
+  const int wl = N == 8 ? 2 : N <= 32 ? 4 : N <= 128 ? 8 : N <= 512 ? 16 : wdst::Geo<1024>::L;
+  const std::vector<double2> wt = lane_tables(wl);
   NTables t;
   cudaError_t e;
   if ((e = cudaMalloc(&t.wtab, sizeof(double2) * (2 * N + 64))) != cudaSuccess) return e;
   cudaMemcpy(t.wtab, wt.data(), sizeof(double2) * (2 * N + 64), cudaMemcpyHostToDevice);
+  if (N == 1024 && wl != 64) {
+    const std::vector<double2> wc = lane_tables(64);
+    if ((e = cudaMalloc(&t.wtab_coop, sizeof(double2) * (2 * N + 64))) != cudaSuccess) return e;
+    cudaMemcpy(t.wtab_coop, wc.data(), sizeof(double2) * (2 * N + 64), cudaMemcpyHostToDevice);
+  }
   if ((e = cudaMalloc(&t.tw, sizeof(double2) * N)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.sj, sizeof(double) * (N + 1))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&t.lam, sizeof(double) * N)) != cudaSuccess) return e;
@@ -1684,7 +1785,7 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
   if (sp.scheme == CHP_LINEAR_A) {
     // whole sweep in one cooperative persistent kernel (no host round trips)
     static int grid_blocks = 0;
-    const size_t smem = sizeof(double) * (256 / wdst::Geo<N>::L) * 2 * N + 16 * (size_t)(N + 64);
+    const size_t smem = CoopGeo<N>::SMEM;
     if (grid_blocks == 0) {
       cudaFuncSetAttribute(k2d_coarse_coop<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
@@ -1703,7 +1804,7 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
     ca.c1 = g.c1; ca.dt = sp.dt; ca.b = sp.b; ca.tol = sp.cg_tol; ca.max_iter = sp.cg_max_iter;
     ca.U = U; ca.F = F; ca.G = G; ca.ics = ics; ca.sls = sls;
     ca.changed = changed; ca.inc = inc; ca.info = info;
-    ca.X = W.X; ca.Rv = W.Rv; ca.Pv = W.Pv; ca.Yv = W.Yv; ca.Cv = W.Cv; ca.CT = W.T2;
+    ca.X = W.X; ca.Rv = W.Rv; ca.Pv = W.Pv; ca.Yv = W.Yv; ca.Cv = W.Cv; ca.CT = W.T2; ca.Mi = W.T1; ca.Dk = W.YH;
     ca.part = W.coop;                    // 2 x 8 doubles per block (alternating)
     ca.bar = reinterpret_cast<unsigned int*>(W.res);
     {
@@ -1715,7 +1816,7 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
       if (env) g_coop_trace = tr;
     }
     cudaMemsetAsync(ca.bar, 0, sizeof(unsigned int), st);
-    ca.lam = nt.lam; ca.wtab = nt.wtab;
+    ca.lam = nt.lam; ca.wtab = (CoopGeo<N>::L == wdst::Geo<N>::L) ? nt.wtab : nt.wtab_coop;
     void* args[] = {&ca};
     return cudaLaunchCooperativeKernel((void*)k2d_coarse_coop<N>, dim3(grid_blocks), dim3(256),
                                        args, smem, st);

@@ -108,10 +108,10 @@ CHP_DEV void load_twiddles(double2* twt, const double2* __restrict__ g) {
 // named barrier of one 64-thread lane group (two warps)
 CHP_DEV void group_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
-// synchronise one lane group (a warp or part of one; two warps for N = 1024)
-template <int N>
+// synchronise one lane group (a warp or part of one; two warps when LG = 64)
+template <int N, int LG = Geo<N>::L>
 CHP_DEV void group_sync() {
-  if constexpr (Geo<N>::L == 64) group_bar(1 + (int)(threadIdx.x / 64));
+  if constexpr (LG == 64) group_bar(1 + (int)(threadIdx.x / 64));
   else __syncwarp();
 }
 
@@ -216,9 +216,11 @@ CHP_DEV void pair_dst64(In in, Out out, double2* scr, const double2* twt, int l,
 //   scr: R*L double2 of group-private shared memory (free when out() runs;
 //        in() must have consumed any data kept there before the transpose);
 //   twt: block-shared twiddle table; ac = (cos, sin)(pi l / N).
-template <int N, class In, class Out>
+//   LG: lanes per group -- Geo<N>::L, or 64 for the two-warp N = 1024 variant
+//        (its own twiddle layout, see the host tables).
+template <int N, int LG = Geo<N>::L, class In, class Out>
 CHP_DEV void pair_dst(In in, Out out, double2* scr, const double2* twt, int l, double2 ac) {
-  if constexpr (Geo<N>::L == 64) {
+  if constexpr (LG == 64) {
     pair_dst64<N>(in, out, scr, twt, l, ac);
     return;
   } else {
