@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libchp.so")
+# CHP_LIB: alternative build of the same library (kernel-variant A/B timing only)
+LIB_PATH = os.environ.get("CHP_LIB") or os.path.join(_HERE, "libchp.so")
 
 CHP_LINEAR_A, CHP_LINEAR_B, CHP_NONLINEAR_EYRE = 0, 1, 2
 SYS_OK, SYS_NEWTON, SYS_NONFINITE, SYS_SINGULAR, SYS_CG = 0, 1, 2, 3, 4

@@ -29,6 +29,7 @@
 #include "chp_common.cuh"
 #include "chp_dst.cuh"
 #include "chp_wdst.cuh"
+#include "chp_linb.cuh"
 
 using chpdst::Tables;
 
@@ -260,6 +261,22 @@ __global__ void k2d_build_dtab(int N, const double* lam, double a2dt, double b, 
   if (p > 0 && q > 0) {
     const double l = lam[p] + lam[q];
     v = scale / ((1.0 - a2dt * l) + b * (l * l));
+  }
+  d[t] = v;
+}
+
+// v2 layout (chp_linb.cuh): [q/2][n] double2 (D(n, q), D(n, q+1)), + 1 slack double2
+__global__ void k2d_build_dtab2(int N, const double* lam, double a2dt, double b, double scale,
+                                double* d) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)N * N + 2) return;
+  double v = 0.0;
+  if (t < (long long)N * N) {
+    const int qp = (int)(t / (2 * N)), n = (int)((t / 2) % N), q = 2 * qp + (int)(t & 1);
+    if (n > 0 && q > 0) {
+      const double l = lam[n] + lam[q];
+      v = scale / ((1.0 - a2dt * l) + b * (l * l));
+    }
   }
   d[t] = v;
 }
@@ -1498,7 +1515,7 @@ struct Chp2d {
   double* host_res = nullptr;     // pinned
   NewtonRec* host_rec = nullptr;  // pinned
   int host_cap = 0;
-  struct DTab { int N; double a2dt, b; double* d; };
+  struct DTab { int N; double a2dt, b, scale; int layout; double* d; };
   std::vector<DTab> dtabs;        // LINEAR_B spectral divisors, one per (N, dt, eps)
 };
 
@@ -1732,26 +1749,66 @@ bool pow2_ok(const chp_grid& g, std::string* err) {
   return true;
 }
 
-cudaError_t get_dtab(Chp2d* c, int N, const chp_spec& sp, const NTables& nt, const double** out,
-                     cudaStream_t st) {
+cudaError_t get_dtab(Chp2d* c, int N, const chp_spec& sp, const NTables& nt, double scale,
+                     int layout, const double** out, cudaStream_t st) {
   const double a2dt = 2.0 * sp.dt, b = sp.b;
   for (auto& t : c->dtabs)
-    if (t.N == N && t.a2dt == a2dt && t.b == b) { *out = t.d; return cudaSuccess; }
+    if (t.N == N && t.a2dt == a2dt && t.b == b && t.scale == scale && t.layout == layout) {
+      *out = t.d;
+      return cudaSuccess;
+    }
   if (c->dtabs.size() >= 8) {              // bounded cache: drop the oldest table
     cudaStreamSynchronize(st);
     cudaFree(c->dtabs.front().d);
     c->dtabs.erase(c->dtabs.begin());
   }
-  Chp2d::DTab t{N, a2dt, b, nullptr};
-  cudaError_t e = cudaMalloc(&t.d, sizeof(double) * (size_t)N * N);
+  Chp2d::DTab t{N, a2dt, b, scale, layout, nullptr};
+  cudaError_t e = cudaMalloc(&t.d, sizeof(double) * ((size_t)N * N + 2));
   if (e != cudaSuccess) return e;
-  const long long n = (long long)N * N;
-  k2d_build_dtab<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(N, nt.lam, a2dt, b,
-                                                            (2.0 / N) * (2.0 / N), t.d);
+  const long long n = (long long)N * N + 2;
+  if (layout == 0)
+    k2d_build_dtab<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(N, nt.lam, a2dt, b, scale, t.d);
+  else
+    k2d_build_dtab2<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(N, nt.lam, a2dt, b, scale, t.d);
   c->dtabs.push_back(t);
   *out = t.d;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   return cudaStreamSynchronize(st);        // usable from any stream afterwards
+}
+
+// LINEAR_B v2 (chp_linb.cuh): J steps = J+1 row passes + J column passes over
+// pair-interleaved P / Q scratch fields (2 N^2 doubles per system).
+template <int N>
+cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int nsys,
+                          const double* in, long long in_stride, double* out, long long out_stride,
+                          const int* sys_index, chp_sys_info* info, const NTables& nt,
+                          double* scratch, const double* dtab, cudaStream_t st) {
+  using RG = linb::RowG<N>;
+  using CG = linb::ColG<N>;
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(linb::k2d_rowb<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
+    cudaFuncSetAttribute(linb::k2d_colb<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
+    attrs = true;
+  }
+  const long long fs2 = (long long)N * N;
+  double* P = scratch;
+  double* Qb = scratch + fs2 * nsys;
+  const dim3 rgrid((RG::NP + RG::SP - 1) / RG::SP, nsys), cgrid(N / CG::TC, nsys);
+  linb::RowArgs ra{};
+  ra.m = g.m; ra.cdt = sp.dt * g.c1; ra.info = info; ra.info_index = sys_index; ra.wtab = nt.wtab;
+  linb::ColArgs ca{Qb, P, fs2, reinterpret_cast<const double2*>(dtab), nt.wtab};
+  for (int s = 0; s < steps; ++s) {
+    if (s == 0) { ra.in = in; ra.in_stride = in_stride; ra.in_index = sys_index; ra.mode = linb::MODE_FIRST; }
+    else { ra.in = P; ra.in_stride = fs2; ra.in_index = nullptr; ra.mode = linb::MODE_MID; }
+    ra.out = Qb; ra.out_stride = fs2; ra.out_index = nullptr;
+    linb::k2d_rowb<N><<<rgrid, RG::THREADS, RG::SMEM, st>>>(ra);
+    linb::k2d_colb<N><<<cgrid, CG::THREADS, CG::SMEM, st>>>(ca);
+  }
+  ra.in = P; ra.in_stride = fs2; ra.in_index = nullptr; ra.mode = linb::MODE_LAST;
+  ra.out = out; ra.out_stride = out_stride; ra.out_index = sys_index;
+  linb::k2d_rowb<N><<<rgrid, RG::THREADS, RG::SMEM, st>>>(ra);
+  return cudaGetLastError();
 }
 
 template <int N>
@@ -1760,11 +1817,17 @@ cudaError_t propagate_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int ste
                         const int* idx, chp_sys_info* info, const NTables& nt, cudaStream_t st) {
   const long long fs = (long long)g.m * N;
   if (sp.scheme == CHP_LINEAR_B) {
+    static const bool v1 = getenv("CHP_LINB_V1") != nullptr;   // A/B: previous passes
     cudaError_t e = grow(reinterpret_cast<void**>(&c->scratch), &c->scratch_bytes,
-                         2 * fs * nsys * sizeof(double), st);
+                         2 * (v1 ? fs : (long long)N * N) * nsys * sizeof(double), st);
     if (e != cudaSuccess) return e;
     const double* dtab = nullptr;
-    if ((e = get_dtab(c, N, sp, nt, &dtab, st)) != cudaSuccess) return e;
+    const double s2 = (2.0 / N) * (2.0 / N);
+    if ((e = get_dtab(c, N, sp, nt, v1 ? s2 : s2 / 256.0, v1 ? 0 : 1, &dtab, st)) != cudaSuccess)
+      return e;
+    if (!v1)
+      return run_linear_b2<N>(g, sp, steps, nsys, in, in_stride, out, out_stride, idx, info, nt,
+                              c->scratch, dtab, st);
     return run_linear_b<N>(g, sp, steps, nsys, in, in_stride, out, out_stride, idx, info, nt,
                            c->scratch, dtab, st);
   }

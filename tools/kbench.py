@@ -68,6 +68,8 @@ def one_d(nx, nsys, scheme, dt, eps, steps):
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     res = []
+    if what == "linb":                       # short case for ncu
+        res.append(linb_2d(1025, 32, 4))
     if what in ("all", "2d"):
         res.append(linb_2d(1025, 64, 16))
         res.append(linb_2d(257, 64, 64))
