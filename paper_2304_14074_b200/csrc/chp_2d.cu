@@ -673,6 +673,7 @@ __global__ void k2d_cg_reduce(int nsys, CgSys* cg, const double* partial, int np
     if (lane == 0) { q.pq = pq; q.alpha = q.rho / pq; }
     return;
   }
+  // modes 0, 2, 4, 5: interleaved (v1, v2) partials
   // modes 0 and 2: interleaved (rho, rr) partials
   double v1 = 0.0, v2 = 0.0;
   const double* p = partial + (long long)s * nparts * 2;
@@ -685,6 +686,12 @@ __global__ void k2d_cg_reduce(int nsys, CgSys* cg, const double* partial, int np
   if (mode == 0) {
     q.rho = v1; q.rr0 = v2; q.rr = v2; q.iters = 0;
     q.done = (v2 == 0.0) ? 1 : 0;
+  } else if (mode == 4) {            // warm start: |b^|^2 is the tolerance reference
+    q.rr0 = v1;
+  } else if (mode == 5) {            // warm start: initial residual of x^0
+    q.rho = v1; q.rr = v2; q.iters = 0;
+    q.done = !(v2 > tol2 * q.rr0) ? 1 : 0;
+    if (!isfinite(v2)) { q.done = 1; q.fail = 1; }
   } else {
     q.beta = v1 / q.rho;
     q.rho = v1;
@@ -813,6 +820,8 @@ __global__ void k2d_cg_collect(int nsys, const CgSys* cg, chp_sys_info* info, co
   info[fi].cg_max = max(info[fi].cg_max, cg[s].iters);
   if (cg[s].fail) atomicCAS(&info[fi].status, CHP_SYS_OK, CHP_SYS_CG);
 }
+
+#include "chp_pcg2.cuh"
 
 __global__ void k2d_newton_norm(int nsys, const double* partial, double hd, double* res,
                                 const int* act) {
@@ -1344,6 +1353,8 @@ __global__ void __launch_bounds__(256, 1) k2d_coarse_coop(CoopArgs a) {
   }
 }
 
+#include "chp_coarse2.cuh"
+
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
@@ -1517,6 +1528,13 @@ struct Chp2d {
   int host_cap = 0;
   struct DTab { int N; double a2dt, b, scale; int layout; double* d; };
   std::vector<DTab> dtabs;        // LINEAR_B spectral divisors, one per (N, dt, eps)
+  void* coarse = nullptr;         // v2 coarse-sweep workspace
+  size_t coarse_bytes = 0;
+  void* pcg = nullptr;            // v2 batched PCG workspace
+  size_t pcg_bytes = 0;
+  double* pcg_tab = nullptr;      // Dk, SK (PI) for (pcg_tab_N, pcg_tab_b)
+  int pcg_tab_N = 0;
+  double pcg_tab_b = 0.0;
 };
 
 Chp2d* chp2d_create() { return new Chp2d(); }
@@ -1533,6 +1551,9 @@ void chp2d_destroy(Chp2d* c) {
   if (c->scratch) cudaFree(c->scratch);
   for (auto& t : c->dtabs) cudaFree(t.d);
   if (c->work) cudaFree(c->work);
+  if (c->coarse) cudaFree(c->coarse);
+  if (c->pcg) cudaFree(c->pcg);
+  if (c->pcg_tab) cudaFree(c->pcg_tab);
   if (c->host_act) cudaFreeHost(c->host_act);
   if (c->host_res) cudaFreeHost(c->host_res);
   if (c->host_rec) cudaFreeHost(c->host_rec);
@@ -1646,6 +1667,103 @@ cudaError_t get_work(Chp2d* c, long long fs, int nsys, Work2* W, cudaStream_t st
   return host_bufs(c, nsys);
 }
 
+// Batched PCG v2 (chp_pcg2.cuh): same contract as pcg_solve (inputs W.RHS,
+// W.Cv, mean(c) partials in W.partial, W.cg[s].active; solution in W.Yv).
+// warm != 0: start from the spectral solution X the previous solve left for the
+// same system (Newton iterate / previous step), with the tolerance still
+// relative to |b^| (the x0 = 0 criterion), which saves CG iterations.
+template <int N>
+cudaError_t pcg_solve2(Chp2d* cx, const chp_grid& g, int nsys, double a, double b, double tol,
+                       int max_iter, const NTables& nt, Work2& W, cudaStream_t st, int warm) {
+  using G2 = Pcg2G<N>;
+  static bool attrs = false;
+  if (!attrs) {
+    const int sm = (int)G2::SMEM;
+    cudaFuncSetAttribute(k_pcg2_rows<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pcg2_rows<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pcg2_rows<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pcg2_cols<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pcg2_cols<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pcg2_cols<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    attrs = true;
+  }
+  const long long NN = (long long)N * N;
+  const double sigma = 1.0 / (8.0 * N);
+  cudaError_t e;
+  if (cx->pcg_tab_N != N || cx->pcg_tab_b != b) {
+    if (cx->pcg_tab) { cudaStreamSynchronize(st); cudaFree(cx->pcg_tab); cx->pcg_tab = nullptr; }
+    if ((e = cudaMalloc(&cx->pcg_tab, sizeof(double) * 2 * NN)) != cudaSuccess) return e;
+    k_pcg2_tables<<<256, 256, 0, st>>>(N, nt.lam, b, sigma, cx->pcg_tab, cx->pcg_tab + NN);
+    cx->pcg_tab_N = N;
+    cx->pcg_tab_b = b;
+  }
+  const size_t per = 5 * (size_t)NN + 2;
+  if (cx->pcg_bytes < sizeof(double) * per * nsys) warm = 0;   // workspace (re)allocated
+  if ((e = grow(&cx->pcg, &cx->pcg_bytes, sizeof(double) * per * nsys, st)) != cudaSuccess) return e;
+  double* w = static_cast<double*>(cx->pcg);
+  Pcg2 p{};
+  p.m = g.m; p.fs = (long long)g.m * N;
+  p.rhs = W.RHS; p.cv = W.Cv; p.out = W.Yv;
+  p.X = w; p.R = w + NN * nsys; p.P = w + 2 * NN * nsys; p.Y = w + 3 * NN * nsys;
+  p.CT = w + 4 * NN * nsys;
+  p.Dk = cx->pcg_tab; p.SK = cx->pcg_tab + NN;
+  p.a = a; p.sigma = sigma; p.cg = W.cg; p.partial = W.partial; p.wtab = nt.wtab;
+  const int red_blocks = (nsys + 7) / 8;
+  const dim3 eg(kPB, nsys), rg(G2::RBLK, nsys), cgd(N / G2::TC, nsys);
+  const size_t sm = G2::SMEM;
+  const int m = g.m;
+  k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 3, 0, 0,
+                                           1.0 / ((double)m * m), a);
+  k_pcg2_prep<N><<<eg, 256, 0, st>>>(p);
+  k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
+  k_pcg2_cols<N, 0><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
+  if (warm) {
+    k_pcg2_warm_a<N><<<eg, 256, 0, st>>>(p);
+    k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 4, 0, 0, 0, 0);
+    k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.P, p.Y, 0);
+    k_pcg2_cols<N, 1><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
+    k_pcg2_rows<N, 2><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
+    k_pcg2_warm_b<N><<<eg, 256, 0, st>>>(p);
+    k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 5, tol * tol, 0, 0, 0);
+  } else {
+    k_pcg2_init<N><<<eg, 256, 0, st>>>(p);
+    k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 0, 0, 0, 0, 0);
+  }
+  const int chunk = 8;
+  std::vector<CgSys> host(nsys);
+  for (int it0 = 0; it0 < max_iter + chunk; it0 += chunk) {
+    for (int it = 0; it < chunk; ++it) {
+      k_pcg2_rows<N, 1><<<rg, G2::THREADS, sm, st>>>(p, nullptr, p.Y, 1);
+      k_pcg2_cols<N, 1><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 1);
+      k_pcg2_rows<N, 2><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 1);
+      k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, G2::RBLK, 1, 0, 0, 0, 0);
+      k_pcg2_update<N><<<eg, 256, 0, st>>>(p);
+      k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 2, tol * tol,
+                                               max_iter, 0, 0);
+    }
+    if ((e = cudaMemcpyAsync(host.data(), W.cg, sizeof(CgSys) * nsys, cudaMemcpyDeviceToHost,
+                             st)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    bool all = true;
+    for (int s = 0; s < nsys; ++s) all = all && (!host[s].active || host[s].done);
+    if (all) break;
+  }
+  // x = S x^ = sigma T'_i T'_j X -> W.Yv (external layout)
+  k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.X, p.Y, 0);
+  k_pcg2_cols<N, 2><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, W.Yv, 0);
+  return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t pcg_dispatch(Chp2d* cx, const chp_grid& g, int nsys, double a, double b, double tol,
+                         int max_iter, const NTables& nt, Work2& W, cudaStream_t st, int warm) {
+  static const bool v1 = getenv("CHP_PCG_V1") != nullptr;   // A/B: previous passes
+  static const bool cold = getenv("CHP_PCG_COLD") != nullptr;
+  if (v1) return pcg_solve<N>(g, nsys, a, b, tol, max_iter, nt, W, st);
+  return pcg_solve2<N>(cx, g, nsys, a, b, tol, max_iter, nt, W, st, cold ? 0 : warm);
+}
+
 // J steps of LINEAR_A (PCG per step) or NONLINEAR_EYRE (Newton + PCG).
 template <int N>
 cudaError_t run_variable(Chp2d* cx, const chp_grid& g, const chp_spec& sp, int steps, int nsys,
@@ -1666,7 +1784,8 @@ cudaError_t run_variable(Chp2d* cx, const chp_grid& g, const chp_spec& sp, int s
       Pt pt{m, N, fs, g.c1, sys_index, sys_index};
       k2d_set_active<<<sb, 128, 0, st>>>(W.cg, nsys, nullptr);
       k2d_prep_a<<<egrid, 256, 0, st>>>(pt, src, sst, W.RHS, W.Cv, sp.dt, W.cg, W.partial);
-      if ((e = pcg_solve<N>(g, nsys, sp.dt, sp.b, tol, maxcg, nt, W, st)) != cudaSuccess) return e;
+      if ((e = pcg_dispatch<N>(cx, g, nsys, sp.dt, sp.b, tol, maxcg, nt, W, st, s > 0)) != cudaSuccess)
+        return e;
       k2d_scatter<<<egrid, 256, 0, st>>>(pt, W.Yv, out, out_stride, W.cg, info, sys_index);
       k2d_cg_collect<<<sb, 128, 0, st>>>(nsys, W.cg, info, sys_index);
     }
@@ -1724,7 +1843,9 @@ cudaError_t run_variable(Chp2d* cx, const chp_grid& g, const chp_spec& sp, int s
       for (int s = 0; s < nsys; ++s) hact[s] = live[s];
       cudaMemcpyAsync(W.act, hact, sizeof(int) * nsys, cudaMemcpyHostToDevice, st);
       k2d_set_active<<<sb, 128, 0, st>>>(W.cg, nsys, W.act);
-      if ((e = pcg_solve<N>(g, nsys, 3.0 * d, b, tol, maxcg, nt, W, st)) != cudaSuccess) return e;
+      if ((e = pcg_dispatch<N>(cx, g, nsys, 3.0 * d, b, tol, maxcg, nt, W, st,
+                               step > 0 || it > 0)) != cudaSuccess)
+        return e;
       k2d_scatter<<<egrid, 256, 0, st>>>(pt, W.Yv, out, out_stride, W.cg, info, sys_index);
       k2d_cg_collect<<<sb, 128, 0, st>>>(nsys, W.cg, info, sys_index);
     }
@@ -1845,6 +1966,50 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
                     long long sls, unsigned char* changed, double* inc, chp_sys_info* info,
                     const NTables& nt, cudaStream_t st) {
   const long long fs = (long long)g.m * N;
+  static const bool coarse_v1 = getenv("CHP_COARSE_V1") != nullptr;   // A/B: previous kernel
+  if (sp.scheme == CHP_LINEAR_A && !coarse_v1) {
+    using G2 = Coop2G<N>;
+    static int blocks = 0;
+    if (blocks == 0) {
+      cudaFuncSetAttribute(k2d_coarse2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)G2::SMEM);
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2d_coarse2<N>, G2::THREADS, G2::SMEM);
+      // one block per SM: enough lane groups for every row pair, and half the
+      // grid-barrier arrivals of two
+      blocks = sms * (per > 0 ? 1 : 1);
+    }
+    const size_t NN = (size_t)N * N;
+    const size_t doubles = 8 * NN + 2 + (size_t)fs + 16 * (size_t)blocks + 16;
+    cudaError_t e = grow(&c->coarse, &c->coarse_bytes, sizeof(double) * doubles, st);
+    if (e != cudaSuccess) return e;
+    double* w = static_cast<double*>(c->coarse);
+    Coop2Args ca{};
+    ca.m = g.m; ca.nic = nic; ca.nsl = nsl; ca.n0 = n0; ca.n1 = n1; ca.mode = mode;
+    ca.c1 = g.c1; ca.dt = sp.dt; ca.b = sp.b; ca.tol = sp.cg_tol; ca.max_iter = sp.cg_max_iter;
+    ca.U = U; ca.F = F; ca.G = G; ca.ics = ics; ca.sls = sls;
+    ca.changed = changed; ca.inc = inc; ca.info = info;
+    ca.X = w; ca.R = w + NN; ca.P = w + 2 * NN; ca.Y = w + 3 * NN; ca.Mi = w + 4 * NN;
+    ca.Dk = w + 5 * NN; ca.SK = w + 6 * NN; ca.CT = w + 7 * NN;       // CT: NN + 2 (slack)
+    ca.gx = w + 8 * NN + 2;
+    ca.part = ca.gx + fs;
+    ca.bar = reinterpret_cast<unsigned int*>(ca.part + 16 * (size_t)blocks);
+    {
+      static unsigned long long* tr = nullptr;
+      const char* env = getenv("CHP_COOP_TRACE");
+      if (env && !tr) cudaMalloc(&tr, sizeof(unsigned long long) * 4096);
+      ca.trace = env ? tr : nullptr;
+      ca.trace_cap = 4096;
+      if (env) g_coop_trace = tr;
+    }
+    cudaMemsetAsync(ca.bar, 0, sizeof(unsigned int), st);
+    ca.lam = nt.lam; ca.wtab = nt.wtab;
+    void* args[] = {&ca};
+    return cudaLaunchCooperativeKernel((void*)k2d_coarse2<N>, dim3(blocks), dim3(G2::THREADS),
+                                       args, G2::SMEM, st);
+  }
   if (sp.scheme == CHP_LINEAR_A) {
     // whole sweep in one cooperative persistent kernel (no host round trips)
     static int grid_blocks = 0;

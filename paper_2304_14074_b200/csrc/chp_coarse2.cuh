@@ -1,0 +1,399 @@
+// Device-resident 2D coarse sweep, v2 (included inside chp_2d.cu's anonymous
+// namespace, after GridBar / coop_block_partials / coop_total).
+//
+// One cooperative persistent kernel runs the whole sequential recursion of
+// parareal.py:245-251 (mode 1) or coarse_init (parareal.py:167-185, mode 0):
+//   for n in [n0, n1):  g = G(U_n)   (LINEAR_A, schemes.py:235-246)
+//                       U_{n+1} = (g + F_n) - G_n ;  G_n = g
+// G solves (I - a L diag(c) + b L^2) x = rhs, c = v^2, a = dt, b = eps^2 dt,
+// as the SPD system (K^-1 + bK + a diag(c)) x = K^-1 rhs in the orthonormal DST
+// basis (x^ = S x, S = (2/N) T_i T_j) by PCG with the diagonal preconditioner
+// M = d + a mean(c), d = 1/kappa + b kappa:
+//   A x^ = d .* x^ + a S (c .* S x^),   b^ = S rhs / kappa.
+// Transforms are chp_fdst.cuh's T' = 4T, so S = sigma T'_i T'_j, sigma = 1/(8N).
+// CG vectors (X, R, P, Y) live in the pair-interleaved layout of chp_linb.cuh
+// (row pairs (2s, 2s+1), N x N doubles, zero pads); c is stored column-pair
+// major ([q/2][n] double2, pre-scaled by a sigma^2) so the column phase applies
+// it coalesced in the inverse transform's pre-processing.
+// Phases per CG iteration (grid barrier after each):
+//   R1  rows: P = M^-1 R + beta P (fused), Y = T'_j P
+//   C   cols: Y = T'_i (c'' .* T'_i Y)
+//   R3  rows: Y = d .* P + T'_j Y,  partial P.Y
+//   U   X += alpha P, R -= alpha Y,  partials R.M^-1 R, R.R
+// Every dot product is a fixed-order two-level reduction: bitwise reproducible.
+
+struct Coop2Args {
+  int m, nic, nsl, n0, n1, mode;
+  double c1, dt, b, tol;
+  int max_iter, pad_;
+  double* U; const double* F; double* G; long long ics, sls;
+  unsigned char* changed; double* inc; chp_sys_info* info;
+  double *X, *R, *P, *Y, *Mi;   // PI layout, N*N each
+  double* Dk;                   // PI: d = 1/kappa + b kappa (constant)
+  double* SK;                   // PI: sigma / kappa (constant)
+  double* CT;                   // [q/2][n] double2: a sigma^2 c(n, q), + slack
+  double* gx;                   // g in the external layout (m x N)
+  double* part;                 // [2][gridDim][8]
+  unsigned int* bar;
+  const double* lam; const double2* wtab;
+  unsigned long long* trace;
+  int trace_cap, pad2_;
+};
+
+template <int N> struct Coop2G {
+  using F = fdst::FG<N>;
+  static constexpr int L = F::L;
+  static constexpr int THREADS = 128;
+  static constexpr int GPB = THREADS / L;                        // lane groups per block
+  static constexpr int GROUPS = (GPB < N / 2) ? GPB : N / 2;     // column pairs per column tile
+  static constexpr int TC = 2 * GROUPS;
+  static constexpr int RBASE(int c) { return c * F::RS + 2 * (c >> 1); }
+  static constexpr size_t SMEM = sizeof(double2) * (size_t)(RBASE(GPB - 1) + F::RS);
+};
+
+// ---- row phase: for every row pair s (grid-strided over lane groups) -------
+//   op 0: out = T' in
+//   op 1: P = (it == 0) ? Mi .* R : Mi .* R + beta P  (written back), out = T' P
+//   op 2: out = Dk .* P + T' in ; returns the thread partial of P . out
+template <int N>
+CHP_DEV double c2_rows(const Coop2Args& a, double2* sm, int op, const double* in, double* out,
+                       int it, double beta) {
+  using F = fdst::FG<N>;
+  using G2 = Coop2G<N>;
+  constexpr int L = F::L, R = F::R, Q = F::Q;
+  const int g = threadIdx.x / L, l = threadIdx.x % L;
+  const int gg = g * gridDim.x + blockIdx.x, ngr = gridDim.x * G2::GPB;
+  double2* reg = sm + G2::RBASE(g);
+  const double2 ac = __ldg(&a.wtab[l]);
+  const double2* twl = a.wtab + N + l;
+  double part = 0.0;
+  for (int s0 = 0; s0 < N / 2; s0 += ngr) {
+    const int s = s0 + gg;
+    const bool have = s < N / 2;              // whole warps iterate together
+    const long long base = (long long)(have ? s : 0) * N;   // double2 index of the pair row
+    if (op == 1) {
+      const double2* Rr = reinterpret_cast<const double2*>(a.R) + base;
+      const double2* Mr = reinterpret_cast<const double2*>(a.Mi) + base;
+      double2* Pr = reinterpret_cast<double2*>(a.P) + base;
+#pragma unroll 8
+      for (int i = 0; i < R; ++i) {
+        const int n = l + L * i;
+        const double2 r = Rr[n], mi = Mr[n];
+        double2 p;
+        if (it == 0) p = make_double2(r.x * mi.x, r.y * mi.y);
+        else {
+          const double2 po = Pr[n];
+          p = make_double2(fma(beta, po.x, r.x * mi.x), fma(beta, po.y, r.y * mi.y));
+        }
+        if (have) Pr[n] = p;
+        reg[n + i / Q] = p;
+      }
+    } else {
+      const double2* src = reinterpret_cast<const double2*>(in) + base;
+#pragma unroll 4
+      for (int i = 0; i < R; ++i) linb::cp16(&reg[l + L * i + i / Q], &src[l + L * i]);
+      linb::cp_wait();
+    }
+    __syncwarp();
+    double2* ob = fdst::out_base<N>(reg, l);
+    fdst::pair_dst<N>(reg, reg, twl, l, 2.0 * ac.y, 2.0 * ac.x,
+                      [&](int j, double a0, double a1, double b0, double b1) {
+                        ob[2 * j] = make_double2(a0, b0);
+                        ob[2 * j + 1] = make_double2(a1, b1);
+                      });
+    __syncwarp();
+    double2* dst = reinterpret_cast<double2*>(out) + base;
+    if (op == 2) {
+      const double2* Pr = reinterpret_cast<const double2*>(a.P) + base;
+      const double2* Dr = reinterpret_cast<const double2*>(a.Dk) + base;
+#pragma unroll 8
+      for (int i = 0; i < R; ++i) {
+        const int n = l + L * i;
+        const double2 y = reg[n + i / Q], p = Pr[n], d = Dr[n];
+        const double2 o = make_double2(fma(d.x, p.x, y.x), fma(d.y, p.y, y.y));
+        if (have) {
+          dst[n] = o;
+          part = fma(p.x, o.x, part);
+          part = fma(p.y, o.y, part);
+        }
+      }
+    } else if (have) {
+#pragma unroll 8
+      for (int i = 0; i < R; ++i) dst[l + L * i] = reg[l + L * i + i / Q];
+    }
+    __syncwarp();
+  }
+  return part;
+}
+
+// ---- column phase: tiles of TC columns (one lane group per column pair) ----
+//   op 0: out = T' in                         (PI -> PI)
+//   op 1: out = T' (CT .* T' in)              (PI -> PI)
+//   op 2: gx = sigma T' in                    (PI -> external layout, rows 1..m)
+template <int N>
+CHP_DEV void c2_cols(const Coop2Args& a, double2* sm, int op, const double* in, double* out,
+                     double sigma) {
+  using F = fdst::FG<N>;
+  using G2 = Coop2G<N>;
+  constexpr int L = F::L, GROUPS = G2::GROUPS, TC = G2::TC;
+  const int g = threadIdx.x / L, l = threadIdx.x % L;
+  const double2 ac = __ldg(&a.wtab[l]);
+  const double2* twl = a.wtab + N + l;
+  double2* reg = sm + G2::RBASE(g);
+  for (int tile = blockIdx.x; tile < N / TC; tile += gridDim.x) {
+    const int j0 = tile * TC;
+    // fill: (pair s, column pair c): 32 contiguous bytes of the PI field
+#pragma unroll 16
+    for (int idx = threadIdx.x; idx < (N / 2) * GROUPS; idx += G2::THREADS) {
+      const int s = idx / GROUPS, c = idx % GROUPS;
+      const double2* src = reinterpret_cast<const double2*>(in + ((long long)s * N + j0 + 2 * c) * 2);
+      const double2 u = src[0], w = src[1];
+      double2* rg = sm + G2::RBASE(c);
+      rg[fdst::p2<N>(2 * s)] = make_double2(u.x, w.x);
+      rg[fdst::p2<N>(2 * s + 1)] = make_double2(u.y, w.y);
+    }
+    __syncthreads();
+    double2* ob = fdst::out_base<N>(reg, l);
+    auto put = [&](int j, double a0, double a1, double b0, double b1) {
+      ob[2 * j] = make_double2(a0, b0);
+      ob[2 * j + 1] = make_double2(a1, b1);
+    };
+    fdst::pair_dst<N>(reg, reg, twl, l, 2.0 * ac.y, 2.0 * ac.x, put);
+    if (op == 1) {
+      __syncwarp();
+      const double2* cr = reinterpret_cast<const double2*>(a.CT) +
+                          (long long)(j0 / 2 + (g < GROUPS ? g : 0)) * N;
+      fdst::pair_dst<N, true>(reg, reg, twl, l, 2.0 * ac.y, 2.0 * ac.x, put, cr + l, cr + N - l);
+    }
+    __syncthreads();
+    if (op == 2) {
+      // external layout: storage row i = math row i + 1; 16 B per (row, column pair)
+      for (int idx = threadIdx.x; idx < a.m * GROUPS; idx += G2::THREADS) {
+        const int i = idx / GROUPS, c = idx % GROUPS;
+        const double2 v = sm[G2::RBASE(c) + fdst::p2<N>(i + 1)];
+        *reinterpret_cast<double2*>(out + (long long)i * N + j0 + 2 * c) =
+            make_double2(v.x * sigma, v.y * sigma);
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < (N / 2) * GROUPS; idx += G2::THREADS) {
+        const int s = idx / GROUPS, c = idx % GROUPS;
+        const double2* rg = sm + G2::RBASE(c);
+        const double2 u = rg[fdst::p2<N>(2 * s)], w = rg[fdst::p2<N>(2 * s + 1)];
+        double2* dst = reinterpret_cast<double2*>(out + ((long long)s * N + j0 + 2 * c) * 2);
+        dst[0] = make_double2(u.x, w.x);
+        dst[1] = make_double2(u.y, w.y);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
+  using G2 = Coop2G<N>;
+  GridBar grid{a.bar, 0u, a.trace, a.trace_cap};
+  extern __shared__ __align__(16) double2 smc2[];
+  __shared__ double red[64];
+  const int m = a.m;
+  const long long NN = (long long)N * N;           // PI field doubles
+  const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gstride = (long long)gridDim.x * blockDim.x;
+  const double sigma = 1.0 / (8.0 * N);
+  const double tol2 = a.tol * a.tol;
+  const double acs = a.dt * sigma * sigma;         // CT scale: a sigma^2
+  // constant tables (PI): Dk = 1/kappa + b kappa, SK = sigma / kappa (zero on pads)
+  for (long long t = gtid; t < NN; t += gstride) {
+    const int s = (int)(t / (2 * N)), q = (int)((t / 2) % N), h = (int)(t & 1);
+    const int p = 2 * s + h;
+    double d = 0.0, sk = 0.0;
+    if (p > 0 && q > 0) {
+      const double kap = -(a.lam[p] + a.lam[q]);
+      d = 1.0 / kap + a.b * kap;
+      sk = sigma / kap;
+    }
+    a.Dk[t] = d;
+    a.SK[t] = sk;
+  }
+  int pb = 0;
+  for (int ic = 0; ic < a.nic; ++ic) {
+    unsigned char* ch = a.changed ? a.changed + (long long)ic * (a.nsl + 1) : nullptr;
+    double* Ui = a.U + ic * a.ics;
+    double* Gi = a.G + ic * a.ics;
+    const double* Fi = a.F ? a.F + ic * a.ics : nullptr;
+    if (a.mode == 1 && (ch[0] & 2)) continue;      // IC frozen
+    double dmax = 0.0;
+    for (int n = a.n0; n < a.n1; ++n) {
+      const double* un = Ui + (long long)n * a.sls;
+      double* un1 = Ui + (long long)(n + 1) * a.sls;
+      double* gn = Gi + (long long)n * a.sls;
+      if (a.mode == 1 && blockIdx.x == 0 && threadIdx.x == 0) ch[n + 1] = 0;
+      gbar(grid);                                   // ch[n] / U_n written by the previous slice
+      const bool solve = (a.mode == 0) || (*(volatile unsigned char*)&ch[n] & 1);
+      if (solve) {
+        // ---- prep: rhs = v - dt L v (PI, into Y), c'' = a sigma^2 v^2 (CT), sum v^2 ----
+        double sc[1] = {0.0};
+        for (long long t = gtid; t < NN / 2; t += gstride) {
+          const int s = (int)(t / N), j = (int)(t % N);
+          double r2[2] = {0.0, 0.0};
+          if (j > 0) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int i = 2 * s + h - 1;          // storage row of math row 2s+h
+              if (i < 0 || i >= m) continue;
+              const long long o = (long long)i * N + j;
+              const double v = un[o];
+              const double vu = i > 0 ? un[o - N] : 0.0, vd = i + 1 < m ? un[o + N] : 0.0;
+              const double vl = j > 1 ? un[o - 1] : 0.0, vr = j < m ? un[o + 1] : 0.0;
+              const double lv = ((((vu * a.c1 + vl * a.c1) + v * (-4.0 * a.c1)) + vr * a.c1) + vd * a.c1);
+              r2[h] = v - a.dt * lv;
+              sc[0] = fma(v, v, sc[0]);
+            }
+          }
+          reinterpret_cast<double2*>(a.Y)[t] = make_double2(r2[0], r2[1]);
+        }
+        for (long long t = gtid; t < NN / 2; t += gstride) {
+          const int qp = (int)(t % (N / 2)), r = (int)(t / (N / 2));   // math row r, columns 2qp, 2qp+1
+          double2 cv = make_double2(0.0, 0.0);
+          if (r > 0) {
+            const double2 v = *reinterpret_cast<const double2*>(un + (long long)(r - 1) * N + 2 * qp);
+            cv = make_double2(qp > 0 ? acs * (v.x * v.x) : 0.0, acs * (v.y * v.y));
+          }
+          reinterpret_cast<double2*>(a.CT)[(long long)qp * N + r] = cv;
+        }
+        double* pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
+        coop_block_partials<1>(sc, red, pbuf);
+        gbar(grid);
+        double tc[1];
+        coop_total<1>(pbuf, red, tc);
+        const double acbar = a.dt * (tc[0] / ((double)m * m));
+        for (long long t = gtid; t < NN; t += gstride) {
+          const double d = a.Dk[t];
+          a.Mi[t] = (d != 0.0) ? 1.0 / (d + acbar) : 0.0;
+        }
+        // ---- b^ = S rhs / kappa: Y = T'_j rhs, Y = T'_i Y, R = SK .* Y in the init ----
+        c2_rows<N>(a, smc2, 0, a.Y, a.Y, 0, 0.0);
+        gbar(grid);
+        c2_cols<N>(a, smc2, 0, a.Y, a.Y, 0.0);
+        gbar(grid);
+        double pr[2] = {0.0, 0.0};
+        {
+          double2* X2 = reinterpret_cast<double2*>(a.X);
+          double2* R2 = reinterpret_cast<double2*>(a.R);
+          const double2* Y2 = reinterpret_cast<const double2*>(a.Y);
+          const double2* S2 = reinterpret_cast<const double2*>(a.SK);
+          const double2* M2 = reinterpret_cast<const double2*>(a.Mi);
+          for (long long t = gtid; t < NN / 2; t += gstride) {
+            const double2 y = Y2[t], sk = S2[t], mi = M2[t];
+            const double2 r = make_double2(y.x * sk.x, y.y * sk.y);
+            X2[t] = make_double2(0.0, 0.0);
+            R2[t] = r;
+            pr[0] = fma(r.x, r.x * mi.x, pr[0]);
+            pr[0] = fma(r.y, r.y * mi.y, pr[0]);
+            pr[1] = fma(r.x, r.x, pr[1]);
+            pr[1] = fma(r.y, r.y, pr[1]);
+          }
+        }
+        pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
+        coop_block_partials<2>(pr, red, pbuf);
+        gbar(grid);
+        double t0[2];
+        coop_total<2>(pbuf, red, t0);
+        double rho = t0[0];
+        const double rr0 = t0[1];
+        int it = 0;
+        bool fail = false;
+        bool done = !(rr0 > 0.0);
+        double beta = 0.0;
+        while (!done) {
+          c2_rows<N>(a, smc2, 1, nullptr, a.Y, it, beta);
+          gbar(grid);
+          c2_cols<N>(a, smc2, 1, a.Y, a.Y, 0.0);
+          gbar(grid);
+          double pq[1];
+          pq[0] = c2_rows<N>(a, smc2, 2, a.Y, a.Y, 0, 0.0);
+          pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
+          coop_block_partials<1>(pq, red, pbuf);
+          gbar(grid);
+          double tq[1];
+          coop_total<1>(pbuf, red, tq);
+          const double alpha = rho / tq[0];
+          double rz[2] = {0.0, 0.0};
+          {
+            double2* X2 = reinterpret_cast<double2*>(a.X);
+            double2* R2 = reinterpret_cast<double2*>(a.R);
+            const double2* P2 = reinterpret_cast<const double2*>(a.P);
+            const double2* Y2 = reinterpret_cast<const double2*>(a.Y);
+            const double2* M2 = reinterpret_cast<const double2*>(a.Mi);
+#pragma unroll 8
+            for (long long t = gtid; t < NN / 2; t += gstride) {
+              double2 xv = X2[t], rv = R2[t];
+              const double2 pv = P2[t], yv = Y2[t], mi = M2[t];
+              xv.x = fma(alpha, pv.x, xv.x);
+              xv.y = fma(alpha, pv.y, xv.y);
+              rv.x = fma(-alpha, yv.x, rv.x);
+              rv.y = fma(-alpha, yv.y, rv.y);
+              X2[t] = xv;
+              R2[t] = rv;
+              rz[0] = fma(rv.x, rv.x * mi.x, rz[0]);
+              rz[0] = fma(rv.y, rv.y * mi.y, rz[0]);
+              rz[1] = fma(rv.x, rv.x, rz[1]);
+              rz[1] = fma(rv.y, rv.y, rz[1]);
+            }
+          }
+          pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
+          coop_block_partials<2>(rz, red, pbuf);
+          gbar(grid);
+          double t1[2];
+          coop_total<2>(pbuf, red, t1);
+          beta = t1[0] / rho;
+          rho = t1[0];
+          ++it;
+          if (!(t1[1] > tol2 * rr0)) done = true;
+          else if (it >= a.max_iter) { done = true; fail = true; }
+          if (!isfinite(t1[1])) { done = true; fail = true; }
+        }
+        if (gtid == 0) {
+          a.info[ic].cg_total += it;
+          a.info[ic].cg_max = max(a.info[ic].cg_max, it);
+          if (fail) atomicCAS(&a.info[ic].status, CHP_SYS_OK, CHP_SYS_CG);
+        }
+        // ---- g = S x^ = sigma T'_i T'_j X -> gx (external layout) -----------------
+        c2_rows<N>(a, smc2, 0, a.X, a.Y, 0, 0.0);
+        gbar(grid);
+        c2_cols<N>(a, smc2, 2, a.Y, a.gx, sigma);
+        gbar(grid);
+      }
+      // ---- correction / init (external layout) ------------------------------------
+      const double* gsrc = solve ? a.gx : gn;
+      const long long tot = (long long)m * N;
+      bool any = false, bad = false;
+      for (long long t = gtid; t < tot; t += gstride) {
+        const int j = (int)(t % N);
+        const double gv = (j > 0) ? gsrc[t] : 0.0;
+        if (a.mode == 0) {
+          un1[t] = gv;
+          gn[t] = gv;
+          bad |= !isfinite(gv);
+          continue;
+        }
+        const double nv = (gv + Fi[(long long)n * a.sls + t]) - gn[t];
+        const double ov = un1[t];
+        any |= (__double_as_longlong(nv) != __double_as_longlong(ov));
+        dmax = fmax(dmax, fabs(nv - ov));
+        bad |= !isfinite(nv) || !isfinite(gv);
+        un1[t] = nv;
+        gn[t] = gv;
+      }
+      if (a.mode == 1) {
+        if (__syncthreads_or(any) && threadIdx.x == 0) ch[n + 1] = 1;
+      }
+      if (__syncthreads_or(bad) && threadIdx.x == 0)
+        atomicCAS(&a.info[ic].status, CHP_SYS_OK, CHP_SYS_NONFINITE);
+    }
+    if (a.mode == 1) {
+      for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+      if ((threadIdx.x & 31) == 0) atomic_max_nonneg(a.inc + ic, dmax);
+    }
+    gbar(grid);
+  }
+}
