@@ -268,7 +268,7 @@ def run_gpu(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                      "peak_source": src,
-                     "kernel": "LINEAR_B fine propagator (k2d_row_pass + k2d_col_pass_b), "
+                     "kernel": "LINEAR_B fine propagator (linb::k2d_rowb + linb::k2d_colb), "
                                "32 B/grid-point-step", "traffic": traffic,
                      "traffic_unit": "DRAM bytes per grid-point-step (ncu, row+column pass)"},
         "clocks": clocks, "gpu_launches": launches * args.steps if launches else launches,

@@ -1966,7 +1966,9 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
                     long long sls, unsigned char* changed, double* inc, chp_sys_info* info,
                     const NTables& nt, cudaStream_t st) {
   const long long fs = (long long)g.m * N;
-  static const bool coarse_v1 = getenv("CHP_COARSE_V1") != nullptr;   // A/B: previous kernel
+  // default: the pair-DST cooperative kernel (chp_coarse2.cuh), 1.5 ms per config-5
+  // slice over a 512-slice sweep; CHP_COARSE_V1 selects the previous kernel (A/B)
+  static const bool coarse_v1 = getenv("CHP_COARSE_V1") != nullptr;
   if (sp.scheme == CHP_LINEAR_A && !coarse_v1) {
     using G2 = Coop2G<N>;
     static int blocks = 0;
