@@ -101,6 +101,7 @@ def coarse_sweep(nx=1025, nsl=8):
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "coarse":
     print(json.dumps(coarse_sweep()), flush=True)
+    print(json.dumps(coarse_sweep(1025, 64)), flush=True)
 
 
 def coarse_trace(nx=1025, nsl=4):
