@@ -1984,7 +1984,7 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
       blocks = sms * (per > 0 ? 1 : 1);
     }
     const size_t NN = (size_t)N * N;
-    const size_t doubles = 8 * NN + 2 + (size_t)fs + 16 * (size_t)blocks + 16;
+    const size_t doubles = 10 * NN + 2 + (size_t)fs + 16 * (size_t)blocks + 16;
     cudaError_t e = grow(&c->coarse, &c->coarse_bytes, sizeof(double) * doubles, st);
     if (e != cudaSuccess) return e;
     double* w = static_cast<double*>(c->coarse);
@@ -1995,7 +1995,8 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
     ca.changed = changed; ca.inc = inc; ca.info = info;
     ca.X = w; ca.R = w + NN; ca.P = w + 2 * NN; ca.Y = w + 3 * NN; ca.Mi = w + 4 * NN;
     ca.Dk = w + 5 * NN; ca.SK = w + 6 * NN; ca.CT = w + 7 * NN;       // CT: NN + 2 (slack)
-    ca.gx = w + 8 * NN + 2;
+    ca.S = w + 8 * NN + 2; ca.W = w + 9 * NN + 2;
+    ca.gx = w + 10 * NN + 2;
     ca.part = ca.gx + fs;
     ca.bar = reinterpret_cast<unsigned int*>(ca.part + 16 * (size_t)blocks);
     {

@@ -15,11 +15,15 @@
 // (row pairs (2s, 2s+1), N x N doubles, zero pads); c is stored column-pair
 // major ([q/2][n] double2, pre-scaled by a sigma^2) so the column phase applies
 // it coalesced in the inverse transform's pre-processing.
-// Phases per CG iteration (grid barrier after each):
-//   R1  rows: P = M^-1 R + beta P (fused), Y = T'_j P
+// CG in the Chronopoulos-Gear form (one reduction per iteration, mathematically
+// the same iterates as standard PCG): with u = M^-1 r, w = A u,
+//   gamma = (r, u), delta = (w, u), beta = gamma / gamma_old,
+//   alpha = gamma / (delta - beta gamma / alpha_old),
+//   p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s.
+// Phases per iteration (grid barrier after each):
+//   R1  rows: p, s, x, r updates fused; u = M^-1 r; Y = T'_j u
 //   C   cols: Y = T'_i (c'' .* T'_i Y)
-//   R3  rows: Y = d .* P + T'_j Y,  partial P.Y
-//   U   X += alpha P, R -= alpha Y,  partials R.M^-1 R, R.R
+//   R3  rows: w = d .* u + T'_j Y; partials gamma, delta, (r, r)
 // Every dot product is a fixed-order two-level reduction: bitwise reproducible.
 
 struct Coop2Args {
@@ -29,6 +33,7 @@ struct Coop2Args {
   double* U; const double* F; double* G; long long ics, sls;
   unsigned char* changed; double* inc; chp_sys_info* info;
   double *X, *R, *P, *Y, *Mi;   // PI layout, N*N each
+  double *S, *W;                // Chronopoulos-Gear: s = A p, w = A u
   double* Dk;                   // PI: d = 1/kappa + b kappa (constant)
   double* SK;                   // PI: sigma / kappa (constant)
   double* CT;                   // [q/2][n] double2: a sigma^2 c(n, q), + slack
@@ -51,13 +56,30 @@ template <int N> struct Coop2G {
   static constexpr size_t SMEM = sizeof(double2) * (size_t)(RBASE(GPB - 1) + F::RS);
 };
 
+// One out-of-line copy of each transform variant for the whole kernel: the
+// phases are latency bound, so a small instruction footprint (every phase
+// runs the same code) and a per-call register budget matter more than inlining.
+template <int N, bool DS>
+__device__ __noinline__ void c2_dst(double2* reg, const double2* __restrict__ twl, int l,
+                                    double sa2, double ca2, const double2* __restrict__ dsc,
+                                    const double2* __restrict__ dsm) {
+  double2* ob = fdst::out_base<N>(reg, l);
+  fdst::pair_dst<N, DS>(reg, reg, twl, l, sa2, ca2,
+                        [&](int j, double a0, double a1, double b0, double b1) {
+                          ob[2 * j] = make_double2(a0, b0);
+                          ob[2 * j + 1] = make_double2(a1, b1);
+                        }, dsc, dsm);
+}
+
 // ---- row phase: for every row pair s (grid-strided over lane groups) -------
 //   op 0: out = T' in
-//   op 1: P = (it == 0) ? Mi .* R : Mi .* R + beta P  (written back), out = T' P
-//   op 2: out = Dk .* P + T' in ; returns the thread partial of P . out
+//   op 3: CG-CG update (p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s,
+//         u = Mi .* r), out = T' u           (first: p = u, s = w)
+//   op 4: W = Dk .* u + T' in (u = Mi .* R); partials (r.u, w.u, r.r) into part[0..2]
+//   op 5: R = SK .* in, X = 0, u = Mi .* R, out = T' u  (CG start, x0 = 0)
 template <int N>
-CHP_DEV double c2_rows(const Coop2Args& a, double2* sm, int op, const double* in, double* out,
-                       int it, double beta) {
+CHP_DEV void c2_rows(const Coop2Args& a, double2* sm, int op, const double* in, double* out,
+                     bool first, double alpha, double beta, double (&part)[3]) {
   using F = fdst::FG<N>;
   using G2 = Coop2G<N>;
   constexpr int L = F::L, R = F::R, Q = F::Q;
@@ -66,27 +88,46 @@ CHP_DEV double c2_rows(const Coop2Args& a, double2* sm, int op, const double* in
   double2* reg = sm + G2::RBASE(g);
   const double2 ac = __ldg(&a.wtab[l]);
   const double2* twl = a.wtab + N + l;
-  double part = 0.0;
   for (int s0 = 0; s0 < N / 2; s0 += ngr) {
     const int s = s0 + gg;
     const bool have = s < N / 2;              // whole warps iterate together
     const long long base = (long long)(have ? s : 0) * N;   // double2 index of the pair row
-    if (op == 1) {
-      const double2* Rr = reinterpret_cast<const double2*>(a.R) + base;
+    if (op == 3 || op == 5) {
+      double2* Rr = reinterpret_cast<double2*>(a.R) + base;
+      double2* Xr = reinterpret_cast<double2*>(a.X) + base;
       const double2* Mr = reinterpret_cast<const double2*>(a.Mi) + base;
       double2* Pr = reinterpret_cast<double2*>(a.P) + base;
-#pragma unroll 8
+      double2* Sr = reinterpret_cast<double2*>(a.S) + base;
+      const double2* Wr = reinterpret_cast<const double2*>(a.W) + base;
+      const double2* Ir = reinterpret_cast<const double2*>(in) + base;
+      const double2* Kr = reinterpret_cast<const double2*>(a.SK) + base;
+#pragma unroll 4
       for (int i = 0; i < R; ++i) {
         const int n = l + L * i;
-        const double2 r = Rr[n], mi = Mr[n];
-        double2 p;
-        if (it == 0) p = make_double2(r.x * mi.x, r.y * mi.y);
-        else {
-          const double2 po = Pr[n];
-          p = make_double2(fma(beta, po.x, r.x * mi.x), fma(beta, po.y, r.y * mi.y));
+        const double2 mi = Mr[n];
+        double2 r, x;
+        if (op == 5) {
+          const double2 y = Ir[n], sk = Kr[n];
+          r = make_double2(y.x * sk.x, y.y * sk.y);
+          x = make_double2(0.0, 0.0);
+        } else {
+          r = Rr[n];
+          x = Xr[n];
+          const double2 w = Wr[n];
+          const double2 u = make_double2(r.x * mi.x, r.y * mi.y);
+          double2 p, sv;
+          if (first) { p = u; sv = w; }
+          else {
+            const double2 po = Pr[n], so = Sr[n];
+            p = make_double2(fma(beta, po.x, u.x), fma(beta, po.y, u.y));
+            sv = make_double2(fma(beta, so.x, w.x), fma(beta, so.y, w.y));
+          }
+          x = make_double2(fma(alpha, p.x, x.x), fma(alpha, p.y, x.y));
+          r = make_double2(fma(-alpha, sv.x, r.x), fma(-alpha, sv.y, r.y));
+          if (have) { Pr[n] = p; Sr[n] = sv; }
         }
-        if (have) Pr[n] = p;
-        reg[n + i / Q] = p;
+        if (have) { Rr[n] = r; Xr[n] = x; }
+        reg[n + i / Q] = make_double2(r.x * mi.x, r.y * mi.y);
       }
     } else {
       const double2* src = reinterpret_cast<const double2*>(in) + base;
@@ -95,35 +136,36 @@ CHP_DEV double c2_rows(const Coop2Args& a, double2* sm, int op, const double* in
       linb::cp_wait();
     }
     __syncwarp();
-    double2* ob = fdst::out_base<N>(reg, l);
-    fdst::pair_dst<N>(reg, reg, twl, l, 2.0 * ac.y, 2.0 * ac.x,
-                      [&](int j, double a0, double a1, double b0, double b1) {
-                        ob[2 * j] = make_double2(a0, b0);
-                        ob[2 * j + 1] = make_double2(a1, b1);
-                      });
+    c2_dst<N, false>(reg, twl, l, 2.0 * ac.y, 2.0 * ac.x, nullptr, nullptr);
     __syncwarp();
-    double2* dst = reinterpret_cast<double2*>(out) + base;
-    if (op == 2) {
-      const double2* Pr = reinterpret_cast<const double2*>(a.P) + base;
+    if (op == 4) {
+      const double2* Rr = reinterpret_cast<const double2*>(a.R) + base;
+      const double2* Mr = reinterpret_cast<const double2*>(a.Mi) + base;
       const double2* Dr = reinterpret_cast<const double2*>(a.Dk) + base;
-#pragma unroll 8
+      double2* Wr = reinterpret_cast<double2*>(a.W) + base;
+#pragma unroll 4
       for (int i = 0; i < R; ++i) {
         const int n = l + L * i;
-        const double2 y = reg[n + i / Q], p = Pr[n], d = Dr[n];
-        const double2 o = make_double2(fma(d.x, p.x, y.x), fma(d.y, p.y, y.y));
+        const double2 y = reg[n + i / Q], r = Rr[n], mi = Mr[n], d = Dr[n];
+        const double2 u = make_double2(r.x * mi.x, r.y * mi.y);
+        const double2 w = make_double2(fma(d.x, u.x, y.x), fma(d.y, u.y, y.y));
         if (have) {
-          dst[n] = o;
-          part = fma(p.x, o.x, part);
-          part = fma(p.y, o.y, part);
+          Wr[n] = w;
+          part[0] = fma(r.x, u.x, part[0]);
+          part[0] = fma(r.y, u.y, part[0]);
+          part[1] = fma(w.x, u.x, part[1]);
+          part[1] = fma(w.y, u.y, part[1]);
+          part[2] = fma(r.x, r.x, part[2]);
+          part[2] = fma(r.y, r.y, part[2]);
         }
       }
     } else if (have) {
+      double2* dst = reinterpret_cast<double2*>(out) + base;
 #pragma unroll 8
       for (int i = 0; i < R; ++i) dst[l + L * i] = reg[l + L * i + i / Q];
     }
     __syncwarp();
   }
-  return part;
 }
 
 // ---- column phase: tiles of TC columns (one lane group per column pair) ----
@@ -153,17 +195,12 @@ CHP_DEV void c2_cols(const Coop2Args& a, double2* sm, int op, const double* in, 
       rg[fdst::p2<N>(2 * s + 1)] = make_double2(u.y, w.y);
     }
     __syncthreads();
-    double2* ob = fdst::out_base<N>(reg, l);
-    auto put = [&](int j, double a0, double a1, double b0, double b1) {
-      ob[2 * j] = make_double2(a0, b0);
-      ob[2 * j + 1] = make_double2(a1, b1);
-    };
-    fdst::pair_dst<N>(reg, reg, twl, l, 2.0 * ac.y, 2.0 * ac.x, put);
+    c2_dst<N, false>(reg, twl, l, 2.0 * ac.y, 2.0 * ac.x, nullptr, nullptr);
     if (op == 1) {
       __syncwarp();
       const double2* cr = reinterpret_cast<const double2*>(a.CT) +
                           (long long)(j0 / 2 + (g < GROUPS ? g : 0)) * N;
-      fdst::pair_dst<N, true>(reg, reg, twl, l, 2.0 * ac.y, 2.0 * ac.x, put, cr + l, cr + N - l);
+      c2_dst<N, true>(reg, twl, l, 2.0 * ac.y, 2.0 * ac.x, cr + l, cr + N - l);
     }
     __syncthreads();
     if (op == 2) {
@@ -270,87 +307,47 @@ __global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
           const double d = a.Dk[t];
           a.Mi[t] = (d != 0.0) ? 1.0 / (d + acbar) : 0.0;
         }
-        // ---- b^ = S rhs / kappa: Y = T'_j rhs, Y = T'_i Y, R = SK .* Y in the init ----
-        c2_rows<N>(a, smc2, 0, a.Y, a.Y, 0, 0.0);
+        // ---- b^ = S rhs / kappa: Y = T'_i T'_j rhs (R = SK .* Y in the start phase) ----
+        double nop[3] = {0.0, 0.0, 0.0};
+        c2_rows<N>(a, smc2, 0, a.Y, a.Y, false, 0.0, 0.0, nop);
         gbar(grid);
         c2_cols<N>(a, smc2, 0, a.Y, a.Y, 0.0);
         gbar(grid);
-        double pr[2] = {0.0, 0.0};
-        {
-          double2* X2 = reinterpret_cast<double2*>(a.X);
-          double2* R2 = reinterpret_cast<double2*>(a.R);
-          const double2* Y2 = reinterpret_cast<const double2*>(a.Y);
-          const double2* S2 = reinterpret_cast<const double2*>(a.SK);
-          const double2* M2 = reinterpret_cast<const double2*>(a.Mi);
-          for (long long t = gtid; t < NN / 2; t += gstride) {
-            const double2 y = Y2[t], sk = S2[t], mi = M2[t];
-            const double2 r = make_double2(y.x * sk.x, y.y * sk.y);
-            X2[t] = make_double2(0.0, 0.0);
-            R2[t] = r;
-            pr[0] = fma(r.x, r.x * mi.x, pr[0]);
-            pr[0] = fma(r.y, r.y * mi.y, pr[0]);
-            pr[1] = fma(r.x, r.x, pr[1]);
-            pr[1] = fma(r.y, r.y, pr[1]);
-          }
-        }
-        pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
-        coop_block_partials<2>(pr, red, pbuf);
+        // ---- start (x0 = 0): r = b^, u = M^-1 r, w = A u; gamma, delta, rr0 ----
+        c2_rows<N>(a, smc2, 5, a.Y, a.Y, true, 0.0, 0.0, nop);
         gbar(grid);
-        double t0[2];
-        coop_total<2>(pbuf, red, t0);
-        double rho = t0[0];
-        const double rr0 = t0[1];
         int it = 0;
-        bool fail = false;
-        bool done = !(rr0 > 0.0);
-        double beta = 0.0;
-        while (!done) {
-          c2_rows<N>(a, smc2, 1, nullptr, a.Y, it, beta);
-          gbar(grid);
+        bool fail = false, done = false, started = false;
+        double alpha = 0.0, beta = 0.0, gamma = 0.0, rr0 = 0.0;
+        for (;;) {
           c2_cols<N>(a, smc2, 1, a.Y, a.Y, 0.0);
           gbar(grid);
-          double pq[1];
-          pq[0] = c2_rows<N>(a, smc2, 2, a.Y, a.Y, 0, 0.0);
-          pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
-          coop_block_partials<1>(pq, red, pbuf);
+          double gd[3] = {0.0, 0.0, 0.0};
+          c2_rows<N>(a, smc2, 4, a.Y, nullptr, false, 0.0, 0.0, gd);
+          double* pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
+          coop_block_partials<3>(gd, red, pbuf);
           gbar(grid);
-          double tq[1];
-          coop_total<1>(pbuf, red, tq);
-          const double alpha = rho / tq[0];
-          double rz[2] = {0.0, 0.0};
-          {
-            double2* X2 = reinterpret_cast<double2*>(a.X);
-            double2* R2 = reinterpret_cast<double2*>(a.R);
-            const double2* P2 = reinterpret_cast<const double2*>(a.P);
-            const double2* Y2 = reinterpret_cast<const double2*>(a.Y);
-            const double2* M2 = reinterpret_cast<const double2*>(a.Mi);
-#pragma unroll 8
-            for (long long t = gtid; t < NN / 2; t += gstride) {
-              double2 xv = X2[t], rv = R2[t];
-              const double2 pv = P2[t], yv = Y2[t], mi = M2[t];
-              xv.x = fma(alpha, pv.x, xv.x);
-              xv.y = fma(alpha, pv.y, xv.y);
-              rv.x = fma(-alpha, yv.x, rv.x);
-              rv.y = fma(-alpha, yv.y, rv.y);
-              X2[t] = xv;
-              R2[t] = rv;
-              rz[0] = fma(rv.x, rv.x * mi.x, rz[0]);
-              rz[0] = fma(rv.y, rv.y * mi.y, rz[0]);
-              rz[1] = fma(rv.x, rv.x, rz[1]);
-              rz[1] = fma(rv.y, rv.y, rz[1]);
-            }
+          double t3[3];
+          coop_total<3>(pbuf, red, t3);
+          const double gam = t3[0], del = t3[1], rr = t3[2];
+          if (!started) {                                // start: alpha0 = gamma0 / delta0
+            started = true;
+            rr0 = rr;
+            done = !(rr0 > 0.0);
+            beta = 0.0;
+            alpha = gam / del;
+          } else {
+            ++it;                                        // x, r of iteration `it` are final
+            if (!(rr > tol2 * rr0)) done = true;         // also stops on NaN
+            else if (it >= a.max_iter) { done = true; fail = true; }
+            if (!isfinite(rr)) { done = true; fail = true; }
+            beta = gam / gamma;
+            alpha = gam / (del - beta * gam / alpha);
           }
-          pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
-          coop_block_partials<2>(rz, red, pbuf);
+          gamma = gam;
+          if (done) break;
+          c2_rows<N>(a, smc2, 3, nullptr, a.Y, it == 0, alpha, beta, nop);
           gbar(grid);
-          double t1[2];
-          coop_total<2>(pbuf, red, t1);
-          beta = t1[0] / rho;
-          rho = t1[0];
-          ++it;
-          if (!(t1[1] > tol2 * rr0)) done = true;
-          else if (it >= a.max_iter) { done = true; fail = true; }
-          if (!isfinite(t1[1])) { done = true; fail = true; }
         }
         if (gtid == 0) {
           a.info[ic].cg_total += it;
@@ -358,7 +355,7 @@ __global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
           if (fail) atomicCAS(&a.info[ic].status, CHP_SYS_OK, CHP_SYS_CG);
         }
         // ---- g = S x^ = sigma T'_i T'_j X -> gx (external layout) -----------------
-        c2_rows<N>(a, smc2, 0, a.X, a.Y, 0, 0.0);
+        c2_rows<N>(a, smc2, 0, a.X, a.Y, false, 0.0, 0.0, nop);
         gbar(grid);
         c2_cols<N>(a, smc2, 2, a.Y, a.gx, sigma);
         gbar(grid);
