@@ -26,6 +26,11 @@
 //   R3  rows: w = d .* u + T'_j Y; partials gamma, delta, (r, r)
 // Every dot product is a fixed-order two-level reduction: bitwise reproducible.
 
+#ifndef CHP_C2_UNROLL
+#define CHP_C2_UNROLL 4
+#endif
+constexpr int kC2U = CHP_C2_UNROLL;   // loads in flight per lane in the elementwise phase parts
+
 struct Coop2Args {
   int m, nic, nsl, n0, n1, mode;
   double c1, dt, b, tol;
@@ -79,14 +84,13 @@ __device__ __noinline__ void c2_dst(double2* reg, const double2* __restrict__ tw
 //   op 5: R = SK .* in, X = 0, u = Mi .* R, out = T' u  (CG start, x0 = 0)
 template <int N>
 CHP_DEV void c2_rows(const Coop2Args& a, double2* sm, int op, const double* in, double* out,
-                     bool first, double alpha, double beta, double (&part)[3]) {
+                     bool first, double alpha, double beta, double2 ac, double (&part)[3]) {
   using F = fdst::FG<N>;
   using G2 = Coop2G<N>;
   constexpr int L = F::L, R = F::R, Q = F::Q;
   const int g = threadIdx.x / L, l = threadIdx.x % L;
   const int gg = g * gridDim.x + blockIdx.x, ngr = gridDim.x * G2::GPB;
   double2* reg = sm + G2::RBASE(g);
-  const double2 ac = __ldg(&a.wtab[l]);
   const double2* twl = a.wtab + N + l;
   for (int s0 = 0; s0 < N / 2; s0 += ngr) {
     const int s = s0 + gg;
@@ -101,7 +105,7 @@ CHP_DEV void c2_rows(const Coop2Args& a, double2* sm, int op, const double* in, 
       const double2* Wr = reinterpret_cast<const double2*>(a.W) + base;
       const double2* Ir = reinterpret_cast<const double2*>(in) + base;
       const double2* Kr = reinterpret_cast<const double2*>(a.SK) + base;
-#pragma unroll 4
+#pragma unroll kC2U
       for (int i = 0; i < R; ++i) {
         const int n = l + L * i;
         const double2 mi = Mr[n];
@@ -143,7 +147,7 @@ CHP_DEV void c2_rows(const Coop2Args& a, double2* sm, int op, const double* in, 
       const double2* Mr = reinterpret_cast<const double2*>(a.Mi) + base;
       const double2* Dr = reinterpret_cast<const double2*>(a.Dk) + base;
       double2* Wr = reinterpret_cast<double2*>(a.W) + base;
-#pragma unroll 4
+#pragma unroll kC2U
       for (int i = 0; i < R; ++i) {
         const int n = l + L * i;
         const double2 y = reg[n + i / Q], r = Rr[n], mi = Mr[n], d = Dr[n];
@@ -174,12 +178,11 @@ CHP_DEV void c2_rows(const Coop2Args& a, double2* sm, int op, const double* in, 
 //   op 2: gx = sigma T' in                    (PI -> external layout, rows 1..m)
 template <int N>
 CHP_DEV void c2_cols(const Coop2Args& a, double2* sm, int op, const double* in, double* out,
-                     double sigma) {
+                     double sigma, double2 ac) {
   using F = fdst::FG<N>;
   using G2 = Coop2G<N>;
   constexpr int L = F::L, GROUPS = G2::GROUPS, TC = G2::TC;
   const int g = threadIdx.x / L, l = threadIdx.x % L;
-  const double2 ac = __ldg(&a.wtab[l]);
   const double2* twl = a.wtab + N + l;
   double2* reg = sm + G2::RBASE(g);
   for (int tile = blockIdx.x; tile < N / TC; tile += gridDim.x) {
@@ -238,6 +241,7 @@ __global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
   const double sigma = 1.0 / (8.0 * N);
   const double tol2 = a.tol * a.tol;
   const double acs = a.dt * sigma * sigma;         // CT scale: a sigma^2
+  const double2 acl = __ldg(&a.wtab[threadIdx.x % fdst::FG<N>::L]);   // per-lane (cos, sin)(pi l / N)
   // constant tables (PI): Dk = 1/kappa + b kappa, SK = sigma / kappa (zero on pads)
   for (long long t = gtid; t < NN; t += gstride) {
     const int s = (int)(t / (2 * N)), q = (int)((t / 2) % N), h = (int)(t & 1);
@@ -309,21 +313,21 @@ __global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
         }
         // ---- b^ = S rhs / kappa: Y = T'_i T'_j rhs (R = SK .* Y in the start phase) ----
         double nop[3] = {0.0, 0.0, 0.0};
-        c2_rows<N>(a, smc2, 0, a.Y, a.Y, false, 0.0, 0.0, nop);
+        c2_rows<N>(a, smc2, 0, a.Y, a.Y, false, 0.0, 0.0, acl, nop);
         gbar(grid);
-        c2_cols<N>(a, smc2, 0, a.Y, a.Y, 0.0);
+        c2_cols<N>(a, smc2, 0, a.Y, a.Y, 0.0, acl);
         gbar(grid);
         // ---- start (x0 = 0): r = b^, u = M^-1 r, w = A u; gamma, delta, rr0 ----
-        c2_rows<N>(a, smc2, 5, a.Y, a.Y, true, 0.0, 0.0, nop);
+        c2_rows<N>(a, smc2, 5, a.Y, a.Y, true, 0.0, 0.0, acl, nop);
         gbar(grid);
         int it = 0;
         bool fail = false, done = false, started = false;
         double alpha = 0.0, beta = 0.0, gamma = 0.0, rr0 = 0.0;
         for (;;) {
-          c2_cols<N>(a, smc2, 1, a.Y, a.Y, 0.0);
+          c2_cols<N>(a, smc2, 1, a.Y, a.Y, 0.0, acl);
           gbar(grid);
           double gd[3] = {0.0, 0.0, 0.0};
-          c2_rows<N>(a, smc2, 4, a.Y, nullptr, false, 0.0, 0.0, gd);
+          c2_rows<N>(a, smc2, 4, a.Y, nullptr, false, 0.0, 0.0, acl, gd);
           double* pbuf = a.part + 8 * gridDim.x * (pb ^= 1);
           coop_block_partials<3>(gd, red, pbuf);
           gbar(grid);
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
           }
           gamma = gam;
           if (done) break;
-          c2_rows<N>(a, smc2, 3, nullptr, a.Y, it == 0, alpha, beta, nop);
+          c2_rows<N>(a, smc2, 3, nullptr, a.Y, it == 0, alpha, beta, acl, nop);
           gbar(grid);
         }
         if (gtid == 0) {
@@ -355,9 +359,9 @@ __global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
           if (fail) atomicCAS(&a.info[ic].status, CHP_SYS_OK, CHP_SYS_CG);
         }
         // ---- g = S x^ = sigma T'_i T'_j X -> gx (external layout) -----------------
-        c2_rows<N>(a, smc2, 0, a.X, a.Y, false, 0.0, 0.0, nop);
+        c2_rows<N>(a, smc2, 0, a.X, a.Y, false, 0.0, 0.0, acl, nop);
         gbar(grid);
-        c2_cols<N>(a, smc2, 2, a.Y, a.gx, sigma);
+        c2_cols<N>(a, smc2, 2, a.Y, a.gx, sigma, acl);
         gbar(grid);
       }
       // ---- correction / init (external layout) ------------------------------------
