@@ -82,12 +82,16 @@ class ShardedParareal:
         self.eng.changed.fill_(1)        # every F(U_n^0) is needed at k = 0
         self.k = 0
 
-    def iterate(self, force_all: bool = False) -> float:
+    def iterate(self, force_all: bool = False, coarse_after=None) -> float:
+        """One Parareal iteration.  ``coarse_after``: an optional CUDA event the
+        coarse sweep waits for (an input copy overlapped with the fine sweep)."""
         eng = self.eng
         flags = eng.changed.cpu().numpy()
         if force_all:
             flags[:, : self.local_slices] |= 1
         eng.fine_sweep(flags)
+        if coarse_after is not None:
+            self._torch.cuda.current_stream().wait_event(coarse_after)
         eng.inc.zero_()
         self._recv_boundary()
         if self.rank == 0:
@@ -133,24 +137,42 @@ class ShardedParareal:
         torch.cuda.synchronize()
         return a.elapsed_time(b)
 
-    def e2e_step_rate(self, steps: int) -> dict:
+    def e2e_step_rate(self, steps: int, warmup: int = 1) -> dict:
         """Same metric with host-resident iterates: per step the local iterates
         and coarse values are copied H2D from pinned memory, one forced
-        iteration runs, and the new iterates are copied back D2H."""
+        iteration runs, and the new iterates are copied back D2H.  The coarse
+        values are only read by the coarse sweep, so their copy runs on a side
+        stream under the fine sweep; the iterates' copies are on the critical
+        path (the fine sweep reads U, the result is U^{k+1})."""
         torch = self._torch
         eng = self.eng
         hU = torch.empty(eng.U.shape, dtype=torch.float64, pin_memory=True)
         hG = torch.empty(eng.G.shape, dtype=torch.float64, pin_memory=True)
+        hOut = torch.empty(eng.U.shape, dtype=torch.float64, pin_memory=True)
         hU.copy_(eng.U)
         hG.copy_(eng.G)
+        side = torch.cuda.Stream(device=eng.U.device)
+        main = torch.cuda.current_stream()
+
+        def step():
+            eng.U.copy_(hU, non_blocking=True)
+            side.wait_stream(main)                    # G is free: the last sweep is done
+            with torch.cuda.stream(side):
+                eng.G.copy_(hG, non_blocking=True)
+                g_ready = torch.cuda.Event()
+                g_ready.record(side)
+            self.iterate(force_all=True, coarse_after=g_ready)
+            # the result U^{k+1} goes to its own buffer: every step starts from the
+            # same consistent host state (U^k, G(U^k))
+            hOut.copy_(eng.U, non_blocking=True)
+
+        for _ in range(warmup):
+            step()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(steps):
-            eng.U.copy_(hU, non_blocking=True)
-            eng.G.copy_(hG, non_blocking=True)
-            self.iterate(force_all=True)
-            hU.copy_(eng.U, non_blocking=True)
+            step()
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / steps
