@@ -105,7 +105,7 @@ def test_linear_b_config5_grid_short(M):
 
 
 @pytest.mark.parametrize("nx,eps,dt", [(9, 0.1, 1e-3), (17, 0.05, 2.0 ** -10), (33, 0.02, 2.0 ** -7),
-                                       (65, 0.015, 2.0 ** -8)])
+                                       (65, 0.015, 2.0 ** -8), (257, 0.02, 2.0 ** -7)])
 def test_linear_a_pcg_vs_reference(M, nx, eps, dt):
     """2D LINEAR_A: matrix-free DST-preconditioned CG vs the reference's SuperLU."""
     G, S, _ = M
@@ -117,8 +117,10 @@ def test_linear_a_pcg_vs_reference(M, nx, eps, dt):
 
 
 @pytest.mark.parametrize("nx,eps,dt", [(17, 0.05, 2.0 ** -12), (33, 0.05, 2.0 ** -12),
-                                       (65, 0.015, 2.0 ** -15)])
+                                       (65, 0.015, 2.0 ** -15), (257, 0.015, 2.0 ** -15)])
 def test_newton_2d_vs_reference(M, nx, eps, dt):
+    """3 Newton steps (steps 2 and 3 warm-start the batched PCG from the previous
+    solve) vs the reference's SuperLU: same Newton counts, <= 1e-10."""
     G, S, _ = M
     g = G.SpatialGrid(2, nx)
     v = np.random.default_rng(nx + 2).uniform(-0.9, 0.9, g.interior_count)
