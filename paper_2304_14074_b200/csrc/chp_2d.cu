@@ -29,18 +29,22 @@ namespace {
 constexpr int kMinN = 8;
 constexpr int kMaxN = 1024;
 
-// v2 layout (chp_linb.cuh): [q/2][n] double2 (D(n, q), D(n, q+1)), + 1 slack double2
-__global__ void k2d_build_dtab2(int N, const double* lam, double a2dt, double b, double scale,
-                                double* d) {
+// LINEAR_B divisors in the column pass's post-processing order (chp_linb.cuh):
+// for column pair qp, lane l of L, r = 2j + h < 2C: (D''(p, 2qp), D''(p, 2qp+1)),
+// p = 2(C l + j) + h, at double2 index qp N + r L + l; zero on the pad row/column.
+__global__ void k2d_build_dtab3(int N, int L, const double* lam, double a2dt, double b,
+                                double scale, double* d) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)N * N + 2) return;
+  if (t >= (long long)N * N) return;
+  const int C = N / (2 * L);
+  const long long e = t / 2;                 // double2 index
+  const int qp = (int)(e / N), w = (int)(e % N), r = w / L, l = w % L;
+  const int p = 2 * (C * l + r / 2) + (r & 1);
+  const int q = 2 * qp + (int)(t & 1);
   double v = 0.0;
-  if (t < (long long)N * N) {
-    const int qp = (int)(t / (2 * N)), n = (int)((t / 2) % N), q = 2 * qp + (int)(t & 1);
-    if (n > 0 && q > 0) {
-      const double l = lam[n] + lam[q];
-      v = scale / ((1.0 - a2dt * l) + b * (l * l));
-    }
+  if (p > 0 && q > 0) {
+    const double x = lam[p] + lam[q];
+    v = scale / ((1.0 - a2dt * x) + b * (x * x));
   }
   d[t] = v;
 }
@@ -814,7 +818,9 @@ cudaError_t get_dtab(Chp2d* c, int N, const chp_spec& sp, const NTables& nt, con
   if (e != cudaSuccess) return e;
   const long long n = (long long)N * N + 2;
   const double scale = (2.0 / N) * (2.0 / N) / 256.0;
-  k2d_build_dtab2<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(N, nt.lam, a2dt, b, scale, t.d);
+  const int lanes = N == 8 ? 2 : N <= 32 ? 4 : N <= 128 ? 8 : N <= 512 ? 16 : 32;   // Geo<N>::L
+  k2d_build_dtab3<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(N, lanes, nt.lam, a2dt, b, scale,
+                                                              t.d);
   c->dtabs.push_back(t);
   *out = t.d;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

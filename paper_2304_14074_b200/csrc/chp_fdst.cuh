@@ -70,11 +70,16 @@ template <int N> CHP_DEV constexpr int p2(int n) { return n + n / FG<N>::R; }
 // dsc (optional): per-row diagonal scale applied to the input (a column pair's
 // spectral divisors, D[n] = (d_a(n), d_b(n)), n = 0..N), read coalesced:
 // dsc points at D + l, dsm at D + N - l.
-template <int N, bool DS = false, class Out>
+// dpo (optional, PS = true): per-output scale, chunk layout: dpo points at
+// T + l, and T[(2j + h) L + l] scales output row 2(C l + j) + h (coalesced; each
+// value read once; the loads are issued after the second DFT so their latency
+// overlaps the post-processing).
+template <int N, bool DS = false, bool PS = false, class Out>
 CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __restrict__ twl, int l,
                       double sa2, double ca2, Out out,
                       const double2* __restrict__ dsc = nullptr,
-                      const double2* __restrict__ dsm = nullptr) {
+                      const double2* __restrict__ dsm = nullptr,
+                      const double2* __restrict__ dpo = nullptr) {
   using G = FG<N>;
   constexpr int L = G::L, R = G::R, Q = G::Q, C = G::C, LB = G::LB, RB = G::RB;
   // Global loads (divisors, twiddles) must not be hoisted across the
@@ -150,6 +155,12 @@ CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __r
     for (int k1 = 0; k1 < L; ++k1) zw[L * t + (R + 2) * k1 + ((Q == 2) ? t : 0)] = v[t][brev(k1, LB)];
   }
   if (l == 0) reg[G::ZN] = v[0][0];               // Z_0 again at zaddr(N)
+  double2 dd[PS ? 2 * C : 1];
+  if constexpr (PS) {
+    asm volatile("" : "+l"(dpo)::"memory");
+#pragma unroll
+    for (int r = 0; r < 2 * C; ++r) dd[r] = __ldcg(dpo + r * L);
+  }
   __syncwarp();
   const double2* xr = reg + (C + 1) * l;
   const double2* yr = reg + (N + 2 * L - 1 - (C + 1) * l);
@@ -179,7 +190,13 @@ CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __r
   const double offa = ia - sa, offb = ib - sb;
   __syncwarp();                                    // Z reads done before out() writes reg
 #pragma unroll
-  for (int j = 0; j < C; ++j) out(j, ea[j], ca[j] + offa, eb[j], cb[j] + offb);
+  for (int j = 0; j < C; ++j) {
+    if constexpr (PS)
+      out(j, ea[j] * dd[2 * j].x, (ca[j] + offa) * dd[2 * j + 1].x, eb[j] * dd[2 * j].y,
+          (cb[j] + offb) * dd[2 * j + 1].y);
+    else
+      out(j, ea[j], ca[j] + offa, eb[j], cb[j] + offb);
+  }
 }
 
 // store the transform output into a pair region in p2 layout (k = C l + j):

@@ -22,8 +22,9 @@
 //             the slot ring has G+1 slots: the last phase-0 pair of a chunk is the
 //             carried halo of the next, so each row is transformed once per phase.
 //   column pass (GROUPS column pairs per block): P = T'_i (D'' .* T'_i Q), the
-//             divisors applied in the second transform's pre-processing from a
-//             table D''[column pair][row] read coalesced
+//             divisors applied in the forward transform's post-processing from a
+//             table laid out in the post-processing's chunk order (coalesced,
+//             each value read once)
 // T' = 4T (chp_fdst.cuh); all normalisations live in D'' = (2/N)^2 D / 256.
 #pragma once
 #include "chp_fdst.cuh"
@@ -265,7 +266,7 @@ struct ColArgs {
   const double* qin;       // Q (row-major, math row i at row i)
   double* pout;            // P (pair-interleaved, pairs (2s, 2s+1))
   long long stride;        // doubles per system (N*N)
-  const double2* dtab;     // [q/2][n] (D''(n, q), D''(n, q+1)), N/2 rows of N (+1 slack)
+  const double2* dtab;     // [q/2][(2j+h) L + l]: (D''(p, q), D''(p, q+1)), p = 2(C l + j) + h
   const double2* wtab;
 };
 
@@ -299,17 +300,16 @@ __global__ void __launch_bounds__(ColG<N>::THREADS, ColG<N>::MINB) k2d_colb(ColA
     const double sa2 = 2.0 * ac.y, ca2 = 2.0 * ac.x;
     const double2* twl = a.wtab + N + l;
     double2* ob = fdst::out_base<N>(reg, l);
-    fdst::pair_dst<N>(reg, reg, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
+    auto put = [&](int j, double a0, double a1, double b0, double b1) {
       ob[2 * j] = make_double2(a0, b0);
       ob[2 * j + 1] = make_double2(a1, b1);
-    });
+    };
+    // D'' of the column pair (j0 + 2g, j0 + 2g + 1) scales the forward transform's
+    // outputs in its post-processing (chunk-layout table, each value read once)
+    const double2* dr = a.dtab + (long long)(j0 / 2 + (g < GROUPS ? g : 0)) * N + l;
+    fdst::pair_dst<N, false, true>(reg, reg, twl, l, sa2, ca2, put, nullptr, nullptr, dr);
     __syncwarp();
-    // D'' of the column pair (j0 + 2g, j0 + 2g + 1), applied to the input of the inverse
-    const double2* dr = a.dtab + (long long)(j0 / 2 + (g < GROUPS ? g : 0)) * N;
-    fdst::pair_dst<N, true>(reg, reg, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
-      ob[2 * j] = make_double2(a0, b0);
-      ob[2 * j + 1] = make_double2(a1, b1);
-    }, dr + l, dr + N - l);
+    fdst::pair_dst<N>(reg, reg, twl, l, sa2, ca2, put);
   }
   __syncthreads();
   // ---- write-out: P pairs (2s, 2s+1), s = 0..N/2-1 -----------------------------
