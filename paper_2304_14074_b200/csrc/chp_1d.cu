@@ -67,8 +67,14 @@ CHP_DEV double div_rn(double x, double d, double r) {
 // written to ub (6 values per row, interleaved stride ks).
 // Returns nonzero if a zero pivot was met (dgbtf2 INFO > 0).
 // ---------------------------------------------------------------------------
+// The rows entering the elimination window are generated kPD rows ahead into a
+// register queue, so the global loads behind gen() (the iterate, yhat) are in
+// flight for kPD elimination steps instead of sitting on the sequential
+// pivot/eliminate chain.  The arithmetic is unchanged (bit-identical).
+constexpr int kPD = 4;
+
 template <class Gen>
-CHP_DEV int band_lu_forward(int m, Gen gen, double* ub, long long ks) {
+CHP_DEV int band_lu_forward(int m, Gen gen, double* __restrict__ ub, long long ks) {
   double W[3][5];
   double bb[3];
 #pragma unroll
@@ -87,73 +93,85 @@ CHP_DEV int band_lu_forward(int m, Gen gen, double* ub, long long ks) {
       bb[r] = rhs;
     }
   }
+  // queue slot q holds row 3 + q (+ kPD per refill)
+  double Qe[kPD][5], Qr[kPD];
+#pragma unroll
+  for (int q = 0; q < kPD; ++q) {
+    const int r = 3 + q;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) Qe[q][c] = 0.0;
+    Qr[q] = 0.0;
+    if (r < m) gen(r, Qe[q], Qr[q]);
+  }
   int singular = 0;
-  #pragma unroll 8
-  for (int j = 0; j < m; ++j) {
-    const int km = min(2, m - 1 - j);
-    int jp = 0;
-    double amax = fabs(W[0][0]);
-    if (km >= 1 && fabs(W[1][0]) > amax) { jp = 1; amax = fabs(W[1][0]); }
-    if (km >= 2 && fabs(W[2][0]) > amax) { jp = 2; }
-    double piv = (jp == 0) ? W[0][0] : (jp == 1 ? W[1][0] : W[2][0]);
-    if (piv != 0.0) {
-      if (jp != 0) {
+  for (int j0 = 0; j0 < m; j0 += kPD) {
 #pragma unroll
-        for (int c = 0; c < 5; ++c) {
-          const double t = W[0][c];
-          W[0][c] = (jp == 1) ? W[1][c] : W[2][c];
-          if (jp == 1) W[1][c] = t; else W[2][c] = t;
+    for (int jj = 0; jj < kPD; ++jj) {
+      const int j = j0 + jj;
+      if (j >= m) break;
+      const int km = min(2, m - 1 - j);
+      int jp = 0;
+      double amax = fabs(W[0][0]);
+      if (km >= 1 && fabs(W[1][0]) > amax) { jp = 1; amax = fabs(W[1][0]); }
+      if (km >= 2 && fabs(W[2][0]) > amax) { jp = 2; }
+      double piv = (jp == 0) ? W[0][0] : (jp == 1 ? W[1][0] : W[2][0]);
+      if (piv != 0.0) {
+        if (jp != 0) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            const double t = W[0][c];
+            W[0][c] = (jp == 1) ? W[1][c] : W[2][c];
+            if (jp == 1) W[1][c] = t; else W[2][c] = t;
+          }
+          const double t = bb[0];
+          bb[0] = (jp == 1) ? bb[1] : bb[2];
+          if (jp == 1) bb[1] = t; else bb[2] = t;
         }
-        const double t = bb[0];
-        bb[0] = (jp == 1) ? bb[1] : bb[2];
-        if (jp == 1) bb[1] = t; else bb[2] = t;
-      }
-      if (km > 0) {
-        const double rcp = 1.0 / W[0][0];           // DSCAL(km, ONE/AB(KV+1,J))
-        W[1][0] = W[1][0] * rcp;
-        if (km >= 2) W[2][0] = W[2][0] * rcp;
+        if (km > 0) {
+          const double rcp = 1.0 / W[0][0];           // DSCAL(km, ONE/AB(KV+1,J))
+          W[1][0] = W[1][0] * rcp;
+          if (km >= 2) W[2][0] = W[2][0] * rcp;
 #pragma unroll
-        for (int c = 1; c < 5; ++c) {               // DGER(-1): fma(l_i, -u_jc, a)
-          W[1][c] = fma(W[1][0], -W[0][c], W[1][c]);
-          if (km >= 2) W[2][c] = fma(W[2][0], -W[0][c], W[2][c]);
+          for (int c = 1; c < 5; ++c) {               // DGER(-1): fma(l_i, -u_jc, a)
+            W[1][c] = fma(W[1][0], -W[0][c], W[1][c]);
+            if (km >= 2) W[2][c] = fma(W[2][0], -W[0][c], W[2][c]);
+          }
+          bb[1] = fma(W[1][0], -bb[0], bb[1]);        // dgbtrs DGER on the rhs
+          if (km >= 2) bb[2] = fma(W[2][0], -bb[0], bb[2]);
         }
-        bb[1] = fma(W[1][0], -bb[0], bb[1]);        // dgbtrs DGER on the rhs
-        if (km >= 2) bb[2] = fma(W[2][0], -bb[0], bb[2]);
+      } else {
+        singular = 1;
       }
-    } else {
-      singular = 1;
-    }
-    double* u = ub + (long long)j * 7 * ks;
+      double* u = ub + (long long)j * 7 * ks;
 #pragma unroll
-    for (int c = 0; c < 5; ++c) u[c * ks] = W[0][c];
-    u[5 * ks] = bb[0];
-    u[6 * ks] = 1.0 / W[0][0];                    // RN(1/U_jj) for the backward sweep
-    // slide the window one row/column down
+      for (int c = 0; c < 5; ++c) u[c * ks] = W[0][c];
+      u[5 * ks] = bb[0];
+      u[6 * ks] = 1.0 / W[0][0];                    // RN(1/U_jj) for the backward sweep
+      // slide the window one row/column down; row j+3 comes from queue slot jj
 #pragma unroll
-    for (int c = 0; c < 4; ++c) { W[0][c] = W[1][c + 1]; W[1][c] = W[2][c + 1]; }
-    W[0][4] = 0.0;
-    W[1][4] = 0.0;
-    bb[0] = bb[1];
-    bb[1] = bb[2];
-    const int r = j + 3;
+      for (int c = 0; c < 4; ++c) { W[0][c] = W[1][c + 1]; W[1][c] = W[2][c + 1]; }
+      W[0][4] = 0.0;
+      W[1][4] = 0.0;
+      bb[0] = bb[1];
+      bb[1] = bb[2];
+      const int r = j + 3;
 #pragma unroll
-    for (int c = 0; c < 5; ++c) W[2][c] = 0.0;
-    bb[2] = 0.0;
-    if (r < m) {
-      double e[5], rhs;
-      gen(r, e, rhs);
+      for (int c = 0; c < 5; ++c)    // window col c <-> matrix col j+1+c = r-2+c
+        W[2][c] = (r < m && r - 2 + c < m) ? Qe[jj][c] : 0.0;
+      bb[2] = (r < m) ? Qr[jj] : 0.0;
+      const int rn = r + kPD;        // refill the slot
 #pragma unroll
-      for (int c = 0; c < 5; ++c) {   // window col c <-> matrix col j+1+c = r-2+c
-        if (r - 2 + c < m) W[2][c] = e[c];
-      }
-      bb[2] = rhs;
+      for (int c = 0; c < 5; ++c) Qe[jj][c] = 0.0;
+      Qr[jj] = 0.0;
+      if (rn < m) gen(rn, Qe[jj], Qr[jj]);
     }
   }
   return singular;
 }
 
 // Upper-triangular band solve (dtbsv 'U','N', bandwidth KL+KU = 4).
-CHP_DEV void band_lu_backward(int m, const double* ub, long long ks, double* x) {
+CHP_DEV void band_lu_backward(int m, const double* __restrict__ ub, long long ks,
+                              double* __restrict__ x) {
   double x1 = 0.0, x2 = 0.0, x3 = 0.0, x4 = 0.0;
   #pragma unroll 8
   for (int i = m - 1; i >= 0; --i) {
