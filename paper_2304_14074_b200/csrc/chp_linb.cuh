@@ -32,6 +32,12 @@
 #ifndef CHP_ROW_WARPS
 #define CHP_ROW_WARPS 4
 #endif
+#ifndef CHP_ROW_MINB
+#define CHP_ROW_MINB 2
+#endif
+#ifndef CHP_COL_WARPS
+#define CHP_COL_WARPS 4
+#endif
 #ifndef CHP_COL_MINB
 #define CHP_COL_MINB 2
 #endif
@@ -49,13 +55,13 @@ template <int N> struct RowG {          // row pass geometry
   static constexpr int CHUNKS = (SP + 1 + G - 1) / G;
   static constexpr int SLOTS = G + 1;
   static constexpr size_t SMEM = sizeof(double2) * (size_t)SLOTS * F::RS;
-  static constexpr int MINB = (N >= 1024) ? 2 : 3;
+  static constexpr int MINB = (N >= 1024) ? CHP_ROW_MINB : 3;
 };
 
 template <int N> struct ColG {          // column pass geometry
   using F = fdst::FG<N>;
   static constexpr int L = F::L;
-  static constexpr int WARPS = (N >= 1024) ? 4 : (N >= 256 ? 4 : 2);
+  static constexpr int WARPS = (N >= 1024) ? CHP_COL_WARPS : (N >= 256 ? 4 : 2);
   static constexpr int THREADS = WARPS * 32;
   static constexpr int GALL = THREADS / L;
   static constexpr int GROUPS = (GALL < N / 2) ? GALL : N / 2;   // column pairs per block
