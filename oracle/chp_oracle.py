@@ -33,6 +33,11 @@ Two knobs make the oracle usable as a like-for-like checker for the GPU:
     DST-I (``scipy.fft.dstn(type=1, norm="ortho")``) -- the exact
     diagonalisation used on the GPU in 2D ("CPU-DST
     oracle").
+``pcg``
+    ``True`` solves the 2D variable-coefficient systems (``LINEAR_A``, the
+    Newton update) by DST-preconditioned CG to 1e-14 instead of SuperLU -- the
+    "PCG ``_solve_shifted``" of the CPU-DST oracle, fast enough for truncated
+    runs at the config-4 grid (SuperLU needs ~18 s per 511^2 solve).
 
 With ``cube="numpy", spectral=False`` the oracle is pinned bit-for-bit against
 golden vectors produced by the unmodified reference (tests/golden/).
@@ -219,9 +224,51 @@ def band_rows(ops: Operators, a: float, b: float, c: np.ndarray) -> np.ndarray:
     return ab
 
 
+def pcg_solve_2d(mesh: Mesh, a: float, b: float, c: np.ndarray, rhs: np.ndarray,
+                 tol: float = 1e-14, max_iter: int = 500) -> np.ndarray:
+    """(I - a L diag(c) + b L^2) x = rhs in 2D by DST-preconditioned CG -- the
+    "PCG _solve_shifted" of the CPU-DST oracle: the SPD form
+    (K^-1 + bK + a diag(c)) x = K^-1 rhs (K = -L) in the orthonormal DST-I
+    basis, preconditioner 1/kappa + b kappa + a mean(c), stop at |r| <= tol |b^|.
+    Plain numpy/scipy.fft; the same algorithm as the GPU's, not its code."""
+    m = mesh.m
+    lam = axis_eigenvalues(mesh.nx)
+    kap = -(lam[:, None] + lam[None, :])
+    d = 1.0 / kap + b * kap
+    cc = c.reshape(m, m)
+
+    def S(x):
+        return sfft.dstn(x, type=1, norm="ortho", workers=-1)
+
+    bh = S(rhs.reshape(m, m)) / kap
+    minv = 1.0 / (d + a * float(cc.mean()))
+    x = np.zeros_like(bh)
+    r = bh.copy()
+    z = minv * r
+    p = z.copy()
+    rz = float(np.sum(r * z))
+    rr0 = float(np.sum(r * r))
+    if rr0 > 0.0:
+        for _ in range(max_iter):
+            q = d * p + a * S(cc * S(p))
+            alpha = rz / float(np.sum(p * q))
+            x += alpha * p
+            r -= alpha * q
+            if not float(np.sum(r * r)) > tol * tol * rr0:
+                break
+            z = minv * r
+            rz_new = float(np.sum(r * z))
+            p = z + (rz_new / rz) * p
+            rz = rz_new
+    return S(x).reshape(-1)
+
+
 def variable_solve(ops: Operators, a: float, b: float, c: np.ndarray,
-                   rhs: np.ndarray) -> np.ndarray:
-    """(I - a L diag(c) + b L^2) x = rhs -- schemes.py:175-188."""
+                   rhs: np.ndarray, pcg: bool = False) -> np.ndarray:
+    """(I - a L diag(c) + b L^2) x = rhs -- schemes.py:175-188 (SuperLU in 2D),
+    or, with ``pcg``, the CPU-DST/PCG oracle solve (2D only)."""
+    if pcg and ops.mesh.dim == 2:
+        return pcg_solve_2d(ops.mesh, a, b, c, rhs)
     if ops.mesh.dim == 1:
         return sla.solve_banded((2, 2), band_rows(ops, a, b, c), rhs,
                                 check_finite=False)
@@ -283,6 +330,7 @@ def constant_solver(ops: Operators, dt: float, eps: float, spectral: bool):
 class Knobs:
     cube: str = "numpy"
     spectral: bool = False
+    pcg: bool = False          # 2D variable-coefficient solves by DST-preconditioned CG
     newton_tol: float = 1e-10
     newton_max_iter: int = 50
 
@@ -308,7 +356,7 @@ def step_a(mesh, v, dt, eps, knobs: Knobs):
     """schemes.py:235-246."""
     ops = operators(mesh)
     rhs = v - dt * (ops.L @ v)
-    return variable_solve(ops, dt, eps ** 2 * dt, v * v, rhs)
+    return variable_solve(ops, dt, eps ** 2 * dt, v * v, rhs, knobs.pcg)
 
 
 def step_b(mesh, v, dt, eps, knobs: Knobs):
@@ -336,7 +384,7 @@ def step_eyre(mesh, u, dt, eps, knobs: Knobs, counter: NewtonCounter | None = No
         if it == knobs.newton_max_iter or not np.isfinite(r):
             raise NewtonFailure(it, r, knobs.newton_tol)
         rhs = yhat - 2.0 * d * (ops.L @ cu)
-        y = variable_solve(ops, 3.0 * d, b, y * y, rhs)
+        y = variable_solve(ops, 3.0 * d, b, y * y, rhs, knobs.pcg)
     raise AssertionError("unreachable")
 
 

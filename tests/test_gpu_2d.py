@@ -184,3 +184,26 @@ def test_config3_truncated_pa3(M):
     ref = O.parareal(O.Mesh(2, 257), u0, "pa3", part.total_time, 4, 128, 0.02, SPECTRAL)
     assert eng.converged_at[0] == ref.k
     assert rel(eng.iterates_host(), ref.iterates) < 1e-10
+
+
+def test_config4_truncated_npa1(M, golden):
+    """Config 4 grid (511^2), eps, fine/coarse steps and seeded u0, first 4 slices
+    (NPA1: Newton fine steps to 1e-10 with the batched PCG, LINEAR_A coarse sweep
+    in the cooperative kernel) against the CPU-DST/PCG oracle
+    (tools/oracle_c4_trunc.py): same k, final iterates within 1e-10, Newton totals
+    equal up to borderline flips."""
+    G, S, P = M
+    z = golden("config4_trunc.npz")
+    g = G.SpatialGrid(2, 513)
+    u0 = O.initial_condition(4)
+    dT = 0.5 / 128
+    part = P.TimePartition(4 * dT, 4, 128)
+    from paper_2304_14074_b200.engine import PararealEngine
+    f, c = P.propagator_pair(P.AlgorithmVariant.NPA1, part, 0.015)
+    eng = PararealEngine(g, f, c, 4, 128)
+    eng.load([G.Field(g, u0)])
+    eng.run()
+    assert eng.converged_at[0] == int(z["k"][0])
+    assert rel(eng.iterates_host()[-1], z["U_end"]) < 1e-10
+    nt = int(z["newton_total"][0])
+    assert abs(eng.newton.total_iterations - nt) <= max(2, nt // 200)

@@ -111,3 +111,17 @@ def test_exact_cube_is_deterministic_and_accurate():
     exact = np.array([float(Fraction(x) ** 3) for x in v])
     assert np.mean(c == exact) > 0.999
     assert np.max(np.abs(c - exact) / np.maximum(np.abs(exact), 1e-300)) <= 2.3e-16
+
+
+def test_oracle_pcg_knob_matches_superlu():
+    """The oracle's 2D DST-PCG solve (Knobs(pcg=True), used for truncated config-4
+    runs) agrees with the reference's SuperLU solve to ~1e-13."""
+    mesh = O.Mesh(2, 65)
+    ops = O.operators(mesh)
+    rng = np.random.default_rng(0)
+    v = rng.uniform(-0.9, 0.9, mesh.size)
+    rhs = rng.uniform(-1.0, 1.0, mesh.size)
+    for a, b in ((2.0 ** -8, 0.02 ** 2 * 2.0 ** -8), (3 * 2.0 ** -15, 0.015 ** 2 * 2.0 ** -15)):
+        x1 = O.variable_solve(ops, a, b, v * v, rhs)
+        x2 = O.variable_solve(ops, a, b, v * v, rhs, pcg=True)
+        assert np.max(np.abs(x1 - x2)) / np.max(np.abs(x1)) < 1e-12
