@@ -45,6 +45,14 @@ class ShardedParareal:
         self.converged_at = None
         self.increments = []
         self._torch = torch
+        self._pending = []              # deferred increment reductions (iterate(defer=True))
+        self._red_group = None
+        if world > 1:
+            # the increment all-reduce runs on its own communicator, so a deferred
+            # reduction of iteration k never queues in front of the boundary
+            # send/recv of iteration k+1 on the chain's communicator
+            import torch.distributed as dist
+            self._red_group = dist.new_group(list(range(world)))
 
     # -- communication helpers ------------------------------------------------
     def _dist(self):
@@ -82,9 +90,13 @@ class ShardedParareal:
         self.eng.changed.fill_(1)        # every F(U_n^0) is needed at k = 0
         self.k = 0
 
-    def iterate(self, force_all: bool = False, coarse_after=None) -> float:
+    def iterate(self, force_all: bool = False, coarse_after=None, defer: bool = False):
         """One Parareal iteration.  ``coarse_after``: an optional CUDA event the
-        coarse sweep waits for (an input copy overlapped with the fine sweep)."""
+        coarse sweep waits for (an input copy overlapped with the fine sweep).
+        ``defer``: do not wait for the all-ranks increment (returns None; call
+        ``flush()``): rank r then starts iteration k+1 as soon as its own part of
+        the coarse chain of iteration k is done, while ranks r+1.. are still in
+        the chain (pipelined Parareal across ranks; same arithmetic)."""
         eng = self.eng
         flags = eng.changed.cpu().numpy()
         if force_all:
@@ -102,14 +114,33 @@ class ShardedParareal:
         self._send_boundary()
         eng.check_status()
         inc = eng.inc.clone()
+        if defer:
+            work = None
+            if self.world > 1:
+                work = self._dist().all_reduce(inc, op=self._dist().ReduceOp.MAX,
+                                               group=self._red_group, async_op=True)
+            self.k += 1
+            self._pending.append((self.k, work, inc))
+            return None
         if self.world > 1:
-            self._dist().all_reduce(inc, op=self._dist().ReduceOp.MAX)
-        val = float(inc[0])
+            self._dist().all_reduce(inc, op=self._dist().ReduceOp.MAX, group=self._red_group)
         self.k += 1
+        return self._record(self.k, inc)
+
+    def _record(self, k, inc) -> float:
+        val = float(inc[0])
         self.increments.append(val)
         if self.converged_at is None and val < self.inc_tol:
-            self.converged_at = self.k
+            self.converged_at = k
         return val
+
+    def flush(self) -> None:
+        """Complete the deferred increment reductions (in iteration order)."""
+        for k, work, inc in self._pending:
+            if work is not None:
+                work.wait()
+            self._record(k, inc)
+        self._pending = []
 
     def run(self, max_iter: int | None = None):
         if max_iter is None:

@@ -108,3 +108,45 @@ def test_shard_bounds():
     assert shard(512, 8, 3) == (192, 256)
     with pytest.raises(ValueError):
         shard(10, 4, 0)
+
+
+def _worker_defer(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2304_14074_b200 import parareal as P
+    from paper_2304_14074_b200.distributed import ShardedParareal
+    from paper_2304_14074_b200.grid import Field, SpatialGrid
+    g = SpatialGrid(1, 17)
+    part = P.TimePartition(0.05, 4, 4)
+    f, c = P.propagator_pair(P.AlgorithmVariant("pa3"), part, 0.1)
+    u0 = np.random.default_rng(3).uniform(-0.5, 0.5, 15)
+    res = []
+    for defer in (False, True):
+        sh = ShardedParareal(g, f, c, 4, 4, rank=rank, world=world, engine_factory=HostEngine)
+        sh.load(Field(g, u0))
+        sh.coarse_init()
+        for _ in range(3):
+            sh.iterate(force_all=True, defer=defer)
+        sh.flush()
+        res.append((sh.k, list(sh.increments), sh.local_iterates()))
+    out_q.put((rank, res))
+    dist.destroy_process_group()
+
+
+def test_two_rank_deferred_increments_match():
+    """iterate(defer=True) (the bench's pipelined step) computes exactly what the
+    synchronous iteration computes: same iterates bit for bit, same increments."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_worker_defer, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, (sync, deferred) in out:
+        assert sync[0] == deferred[0] == 3
+        assert sync[1] == deferred[1]
+        assert np.array_equal(sync[2], deferred[2])
