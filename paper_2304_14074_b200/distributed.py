@@ -192,18 +192,20 @@ class ShardedParareal:
                 eng.G.copy_(hG, non_blocking=True)
                 g_ready = torch.cuda.Event()
                 g_ready.record(side)
-            self.iterate(force_all=True, coarse_after=g_ready)
+            self.iterate(force_all=True, coarse_after=g_ready, defer=True)
             # the result U^{k+1} goes to its own buffer: every step starts from the
             # same consistent host state (U^k, G(U^k))
             hOut.copy_(eng.U, non_blocking=True)
 
         for _ in range(warmup):
             step()
+        self.flush()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(steps):
             step()
+        self.flush()
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / steps
