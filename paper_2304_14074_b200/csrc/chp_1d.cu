@@ -67,16 +67,24 @@ CHP_DEV double div_rn(double x, double d, double r) {
 // written to ub (6 values per row, interleaved stride ks).
 // Returns nonzero if a zero pivot was met (dgbtf2 INFO > 0).
 // ---------------------------------------------------------------------------
-// The rows entering the elimination window are generated kPD rows ahead into a
-// register queue, so the global loads behind gen() (the iterate, yhat) are in
-// flight for kPD elimination steps instead of sitting on the sequential
-// pivot/eliminate chain.  The arithmetic is unchanged (bit-identical).
-constexpr int kPD = 4;
+// The raw inputs of the rows entering the elimination window (the iterate value
+// y_{r+1} and a per-row auxiliary such as yhat_r) are loaded kPD rows ahead
+// into a register queue; the row itself is formed only when it enters, so the
+// global loads are in flight for kPD elimination steps instead of sitting on
+// the sequential pivot/eliminate chain.  The arithmetic is unchanged (the row
+// is formed from the same values with the same expressions: bit-identical).
+//   load(r)                      -> double2 (y_{r+1} or 0, aux_r or 0)
+//   make(r, ym, y0, yp, aux, e[5], rhs)  row r from y_{r-1}, y_r, y_{r+1}, aux_r
+constexpr int kPD = 8;
 
-template <class Gen>
-CHP_DEV int band_lu_forward(int m, Gen gen, double* __restrict__ ub, long long ks) {
+template <class Load, class Make>
+CHP_DEV int band_lu_forward(int m, Load load, Make make, double* __restrict__ ub, long long ks) {
   double W[3][5];
   double bb[3];
+  // rows 0..2 directly; y window for row 3 = (y_2, y_3)
+  double yv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) yv[i] = (i < m) ? load(i - 1).x : 0.0;   // load(i-1).x = y_i
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
 #pragma unroll
@@ -84,7 +92,7 @@ CHP_DEV int band_lu_forward(int m, Gen gen, double* __restrict__ ub, long long k
     bb[r] = 0.0;
     if (r < m) {
       double e[5], rhs;
-      gen(r, e, rhs);
+      make(r, r >= 1 ? yv[r - 1] : 0.0, yv[r], yv[r + 1], load(r).y, e, rhs);
 #pragma unroll
       for (int d = -2; d <= 2; ++d) {
         const int col = r + d;
@@ -93,16 +101,10 @@ CHP_DEV int band_lu_forward(int m, Gen gen, double* __restrict__ ub, long long k
       bb[r] = rhs;
     }
   }
-  // queue slot q holds row 3 + q (+ kPD per refill)
-  double Qe[kPD][5], Qr[kPD];
+  double w0 = yv[2], w1 = yv[3];
+  double2 Qy[kPD];
 #pragma unroll
-  for (int q = 0; q < kPD; ++q) {
-    const int r = 3 + q;
-#pragma unroll
-    for (int c = 0; c < 5; ++c) Qe[q][c] = 0.0;
-    Qr[q] = 0.0;
-    if (r < m) gen(r, Qe[q], Qr[q]);
-  }
+  for (int q = 0; q < kPD; ++q) Qy[q] = load(3 + q);
   int singular = 0;
   for (int j0 = 0; j0 < m; j0 += kPD) {
 #pragma unroll
@@ -147,7 +149,7 @@ CHP_DEV int band_lu_forward(int m, Gen gen, double* __restrict__ ub, long long k
       for (int c = 0; c < 5; ++c) u[c * ks] = W[0][c];
       u[5 * ks] = bb[0];
       u[6 * ks] = 1.0 / W[0][0];                    // RN(1/U_jj) for the backward sweep
-      // slide the window one row/column down; row j+3 comes from queue slot jj
+      // slide the window one row/column down; row r = j+3 enters from the queue
 #pragma unroll
       for (int c = 0; c < 4; ++c) { W[0][c] = W[1][c + 1]; W[1][c] = W[2][c + 1]; }
       W[0][4] = 0.0;
@@ -155,15 +157,21 @@ CHP_DEV int band_lu_forward(int m, Gen gen, double* __restrict__ ub, long long k
       bb[0] = bb[1];
       bb[1] = bb[2];
       const int r = j + 3;
+      const double2 q = Qy[jj];
 #pragma unroll
-      for (int c = 0; c < 5; ++c)    // window col c <-> matrix col j+1+c = r-2+c
-        W[2][c] = (r < m && r - 2 + c < m) ? Qe[jj][c] : 0.0;
-      bb[2] = (r < m) ? Qr[jj] : 0.0;
-      const int rn = r + kPD;        // refill the slot
+      for (int c = 0; c < 5; ++c) W[2][c] = 0.0;
+      bb[2] = 0.0;
+      if (r < m) {
+        double e[5], rhs;
+        make(r, w0, w1, q.x, q.y, e, rhs);
 #pragma unroll
-      for (int c = 0; c < 5; ++c) Qe[jj][c] = 0.0;
-      Qr[jj] = 0.0;
-      if (rn < m) gen(rn, Qe[jj], Qr[jj]);
+        for (int c = 0; c < 5; ++c)  // window col c <-> matrix col j+1+c = r-2+c
+          if (r - 2 + c < m) W[2][c] = e[c];
+        bb[2] = rhs;
+      }
+      w0 = w1;
+      w1 = q.x;
+      Qy[jj] = load(r + kPD);        // refill: row r + kPD
     }
   }
   return singular;
@@ -224,12 +232,12 @@ CHP_DEV int step_linear_a(const G1& g, double dt, double b, const double* src, d
                           double* ub, long long ks) {
   const int m = g.m;
   const BandConst k = band_const(dt, b, g);
-  auto gen = [&](int r, double e[5], double& rhs) {
-    const double vm = ld(src, r - 1, m), v0 = src[r], vp = ld(src, r + 1, m);
+  auto load = [&](int r) { return make_double2(ld(src, r + 1, m), 0.0); };
+  auto make = [&](int r, double vm, double v0, double vp, double, double e[5], double& rhs) {
     band_row(r, m, k, vm * vm, v0 * v0, vp * vp, e);
     rhs = v0 - dt * lap3(vm, v0, vp, g.c1);
   };
-  const int sing = band_lu_forward(m, gen, ub, ks);
+  const int sing = band_lu_forward(m, load, make, ub, ks);
   band_lu_backward(m, ub, ks, dst);
   return sing;
 }
@@ -321,14 +329,18 @@ CHP_DEV int step_eyre(const G1& g, double d, double b, double tol, int maxit,
       return CHP_SYS_NEWTON;
     }
     // (I + b L^2 - 3d L diag(y^2)) y_new = yhat - 2d L y^3   (schemes.py:303-304)
-    auto gen = [&](int rr, double e[5], double& rhs) {
-      const double ym = ld(y, rr - 1, m), y0 = y[rr], yp = ld(y, rr + 1, m);
+    auto load = [&](int rr) {
+      return make_double2(ld(y, rr + 1, m),
+                          (rr >= 0 && rr < m) ? yh[(long long)rr * ks] : 0.0);
+    };
+    auto make = [&](int rr, double ym, double y0, double yp, double yhr, double e[5],
+                    double& rhs) {
       band_row(rr, m, k, ym * ym, y0 * y0, yp * yp, e);
       const double cm = (rr >= 1) ? chp_cube(ym) : 0.0;
       const double cp = (rr + 1 < m) ? chp_cube(yp) : 0.0;
-      rhs = yh[(long long)rr * ks] - d2 * lap3(cm, chp_cube(y0), cp, g.c1);
+      rhs = yhr - d2 * lap3(cm, chp_cube(y0), cp, g.c1);
     };
-    if (band_lu_forward(m, gen, ub, ks)) return CHP_SYS_SINGULAR;
+    if (band_lu_forward(m, load, make, ub, ks)) return CHP_SYS_SINGULAR;
     band_lu_backward(m, ub, ks, y);
   }
   return CHP_SYS_NEWTON;  // unreachable
