@@ -180,18 +180,34 @@ CHP_DEV int band_lu_forward(int m, Load load, Make make, double* __restrict__ ub
 // Upper-triangular band solve (dtbsv 'U','N', bandwidth KL+KU = 4).
 CHP_DEV void band_lu_backward(int m, const double* __restrict__ ub, long long ks,
                               double* __restrict__ x) {
+  // the 7 values of row i are loaded kPB rows ahead into a register queue
+  constexpr int kPB = 4;
+  double Q[kPB][7];
+  auto fetch = [&](int i, double (&q)[7]) {
+    if (i >= 0) {
+      const double* u = ub + (long long)i * 7 * ks;
+#pragma unroll
+      for (int c = 0; c < 7; ++c) q[c] = u[c * ks];
+    }
+  };
+#pragma unroll
+  for (int p = 0; p < kPB; ++p) fetch(m - 1 - p, Q[p]);
   double x1 = 0.0, x2 = 0.0, x3 = 0.0, x4 = 0.0;
-  #pragma unroll 8
-  for (int i = m - 1; i >= 0; --i) {
-    const double* u = ub + (long long)i * 7 * ks;
-    double t = u[5 * ks];
-    t = fma(-x4, u[4 * ks], t);
-    t = fma(-x3, u[3 * ks], t);
-    t = fma(-x2, u[2 * ks], t);
-    t = fma(-x1, u[1 * ks], t);
-    const double xi = div_rn(t, u[0], u[6 * ks]);
-    x4 = x3; x3 = x2; x2 = x1; x1 = xi;
-    x[i] = xi;
+  for (int i0 = m - 1; i0 >= 0; i0 -= kPB) {
+#pragma unroll
+    for (int p = 0; p < kPB; ++p) {
+      const int i = i0 - p;
+      if (i < 0) break;
+      double t = Q[p][5];
+      t = fma(-x4, Q[p][4], t);
+      t = fma(-x3, Q[p][3], t);
+      t = fma(-x2, Q[p][2], t);
+      t = fma(-x1, Q[p][1], t);
+      const double xi = div_rn(t, Q[p][0], Q[p][6]);
+      x4 = x3; x3 = x2; x2 = x1; x1 = xi;
+      x[i] = xi;
+      fetch(i - kPB, Q[p]);
+    }
   }
 }
 
