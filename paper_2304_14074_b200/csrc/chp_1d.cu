@@ -178,8 +178,11 @@ CHP_DEV int band_lu_forward(int m, Load load, Make make, double* __restrict__ ub
 }
 
 // Upper-triangular band solve (dtbsv 'U','N', bandwidth KL+KU = 4).
-CHP_DEV void band_lu_backward(int m, const double* __restrict__ ub, long long ks,
+// Returns whether every x_i is finite (checked on the values as they are
+// produced: the Field validation of grid.py:84-85 without re-reading x).
+CHP_DEV bool band_lu_backward(int m, const double* __restrict__ ub, long long ks,
                               double* __restrict__ x) {
+  bool fin = true;
   // the 7 values of row i are loaded kPB rows ahead into a register queue
   constexpr int kPB = 4;
   double Q[kPB][7];
@@ -206,9 +209,11 @@ CHP_DEV void band_lu_backward(int m, const double* __restrict__ ub, long long ks
       const double xi = div_rn(t, Q[p][0], Q[p][6]);
       x4 = x3; x3 = x2; x2 = x1; x1 = xi;
       x[i] = xi;
+      fin = fin && isfinite(xi);
       fetch(i - kPB, Q[p]);
     }
   }
+  return fin;
 }
 
 struct BandConst {   // scalars of I - a L diag(c) + b L^2 (schemes.py:149-153)
@@ -254,13 +259,13 @@ CHP_DEV int step_linear_a(const G1& g, double dt, double b, const double* src, d
     rhs = v0 - dt * lap3(vm, v0, vp, g.c1);
   };
   const int sing = band_lu_forward(m, load, make, ub, ks);
-  band_lu_backward(m, ub, ks, dst);
-  return sing;
+  const bool fin = band_lu_backward(m, ub, ks, dst);
+  return sing ? CHP_SYS_SINGULAR : (fin ? CHP_SYS_OK : CHP_SYS_NONFINITE);
 }
 
 // LINEAR_B with the cached Cholesky factor fac = [F0 | F1 | F2] (3*m):
 // F2 = diagonal of U, F1[i] = U[i-1,i], F0[i] = U[i-2,i]  (LAPACK 'U' band).
-CHP_DEV void step_linear_b(const G1& g, double dt, const double* __restrict__ fac,
+CHP_DEV bool step_linear_b(const G1& g, double dt, const double* __restrict__ fac,
                            const double* src, double* dst, double* yb, long long ks) {
   const int m = g.m;
   const double* F0 = fac;
@@ -287,6 +292,7 @@ CHP_DEV void step_linear_b(const G1& g, double dt, const double* __restrict__ fa
   }
   // backward: U x = y (dtbsv 'U','N': divide then axpy)
   double x1 = 0.0, x2 = 0.0;
+  bool fin = true;
   #pragma unroll 8
   for (int i = m - 1; i >= 0; --i) {
     double t = yb[(long long)i * ks];
@@ -295,7 +301,9 @@ CHP_DEV void step_linear_b(const G1& g, double dt, const double* __restrict__ fa
     const double xi = div_rn(t, F2[i], R2[i]);
     x2 = x1; x1 = xi;
     dst[i] = xi;
+    fin = fin && isfinite(xi);
   }
+  return fin;
 }
 
 // EYRE: Newton on H(Y) = Y + b L^2 Y - d L Y^3 - yhat, yhat = u - d L u.
@@ -357,15 +365,9 @@ CHP_DEV int step_eyre(const G1& g, double d, double b, double tol, int maxit,
       rhs = yhr - d2 * lap3(cm, chp_cube(y0), cp, g.c1);
     };
     if (band_lu_forward(m, load, make, ub, ks)) return CHP_SYS_SINGULAR;
-    band_lu_backward(m, ub, ks, y);
+    (void)band_lu_backward(m, ub, ks, y);   // a non-finite y makes the next residual non-finite
   }
   return CHP_SYS_NEWTON;  // unreachable
-}
-
-CHP_DEV bool all_finite(const double* x, int m) {
-  bool ok = true;
-  for (int i = 0; i < m; ++i) ok = ok && isfinite(x[i]);
-  return ok;
 }
 
 struct Scratch1 {   // per-launch interleaved scratch
@@ -382,10 +384,12 @@ CHP_DEV int one_step(const G1& g, const chp_spec& sp, const double* fac, const d
   double* ub = S.ub + t;
   double* yh = S.yh + t;
   if (sp.scheme == CHP_LINEAR_B) {
-    step_linear_b(g, sp.dt, fac, src, dst, yh, S.ks);
+    if (!step_linear_b(g, sp.dt, fac, src, dst, yh, S.ks)) st = CHP_SYS_NONFINITE;
   } else if (sp.scheme == CHP_LINEAR_A) {
-    if (step_linear_a(g, sp.dt, sp.b, src, dst, ub, S.ks)) st = CHP_SYS_SINGULAR;
+    st = step_linear_a(g, sp.dt, sp.b, src, dst, ub, S.ks);
   } else {
+    // EYRE: an accepted step has a finite residual, hence a finite iterate
+    // (schemes.py:287-302 raises before the Field check otherwise)
     int it = 0;
     double r = 0.0;
     st = step_eyre(g, sp.dt, sp.b, sp.newton_tol, sp.newton_max_iter, src, dst, yh, ub, S.ks,
@@ -403,10 +407,6 @@ CHP_DEV int one_step(const G1& g, const chp_spec& sp, const double* fac, const d
   if (st != CHP_SYS_OK) {
     sysinfo_fail(info, st, 0, 0.0);
     return st;
-  }
-  if (!all_finite(dst, g.m)) {
-    sysinfo_fail(info, CHP_SYS_NONFINITE, 0, 0.0);
-    return CHP_SYS_NONFINITE;
   }
   return CHP_SYS_OK;
 }
