@@ -177,42 +177,65 @@ CHP_DEV int band_lu_forward(int m, Load load, Make make, double* __restrict__ ub
   return singular;
 }
 
+// cp.async helpers and the per-lane shared ring of the backward sweep
+#ifndef CHP_1D_RB
+#define CHP_1D_RB 16
+#endif
+constexpr int kRB = CHP_1D_RB;
+constexpr int kRingBytes = kRB * 7 * 32 * (int)sizeof(double);
+static_assert(kRingBytes <= 48 * 1024, "default dynamic shared memory limit");
+
+CHP_DEV void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+CHP_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+CHP_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // Upper-triangular band solve (dtbsv 'U','N', bandwidth KL+KU = 4).
 // Returns whether every x_i is finite (checked on the values as they are
 // produced: the Field validation of grid.py:84-85 without re-reading x).
 CHP_DEV bool band_lu_backward(int m, const double* __restrict__ ub, long long ks,
                               double* __restrict__ x) {
   bool fin = true;
-  // the 7 values of row i are loaded kPB rows ahead into a register queue
-  constexpr int kPB = 4;
-  double Q[kPB][7];
-  auto fetch = [&](int i, double (&q)[7]) {
+  // The 7 values of row i are staged kRB rows ahead into a per-lane shared
+  // ring by cp.async: the prefetch depth costs no registers, so the chain of
+  // dependent divides never waits on the L2 round trip of the ub rows that
+  // the forward sweep has just written.  Launches are one warp per block.
+  // The ring is dynamic shared memory (kRingBytes) so that LINEAR_B launches,
+  // which never reach this sweep, keep the whole L1 carve-out.
+  extern __shared__ double ring1d[];
+  double(*ring)[7][32] = reinterpret_cast<double (*)[7][32]>(ring1d);
+  const int lane = threadIdx.x & 31;
+  auto issue = [&](int i) {
     if (i >= 0) {
       const double* u = ub + (long long)i * 7 * ks;
+      double* s = &ring[i & (kRB - 1)][0][lane];
 #pragma unroll
-      for (int c = 0; c < 7; ++c) q[c] = u[c * ks];
+      for (int c = 0; c < 7; ++c) cp_async8(s + c * 32, u + c * ks);
     }
+    cp_commit();
   };
 #pragma unroll
-  for (int p = 0; p < kPB; ++p) fetch(m - 1 - p, Q[p]);
+  for (int p = 0; p < kRB; ++p) issue(m - 1 - p);
   double x1 = 0.0, x2 = 0.0, x3 = 0.0, x4 = 0.0;
-  for (int i0 = m - 1; i0 >= 0; i0 -= kPB) {
-#pragma unroll
-    for (int p = 0; p < kPB; ++p) {
-      const int i = i0 - p;
-      if (i < 0) break;
-      double t = Q[p][5];
-      t = fma(-x4, Q[p][4], t);
-      t = fma(-x3, Q[p][3], t);
-      t = fma(-x2, Q[p][2], t);
-      t = fma(-x1, Q[p][1], t);
-      const double xi = div_rn(t, Q[p][0], Q[p][6]);
-      x4 = x3; x3 = x2; x2 = x1; x1 = xi;
-      x[i] = xi;
-      fin = fin && isfinite(xi);
-      fetch(i - kPB, Q[p]);
-    }
+#pragma unroll 4
+  for (int i = m - 1; i >= 0; --i) {
+    cp_wait<kRB - 1>();
+    const double* q = &ring[i & (kRB - 1)][0][lane];
+    double t = q[5 * 32];
+    t = fma(-x4, q[4 * 32], t);
+    t = fma(-x3, q[3 * 32], t);
+    t = fma(-x2, q[2 * 32], t);
+    t = fma(-x1, q[1 * 32], t);
+    const double xi = div_rn(t, q[0], q[6 * 32]);
+    x4 = x3; x3 = x2; x2 = x1; x1 = xi;
+    x[i] = xi;
+    fin = fin && isfinite(xi);
+    issue(i - kRB);   // same slot: its values were consumed by the chain above
   }
+  cp_wait<0>();
   return fin;
 }
 
@@ -557,7 +580,8 @@ cudaError_t chp1d_propagate(const chp_grid& g, const chp_spec& sp, int steps, in
                             cudaStream_t st) {
   Scratch1 S{ub, yh, tmp, nsys};
   const int bs = 32;
-  k1d_propagate<<<(nsys + bs - 1) / bs, bs, 0, st>>>(g, sp, steps, nsys, in, in_stride, out,
+  const int smem = sp.scheme == CHP_LINEAR_B ? 0 : kRingBytes;
+  k1d_propagate<<<(nsys + bs - 1) / bs, bs, smem, st>>>(g, sp, steps, nsys, in, in_stride, out,
                                                      out_stride, sys_index, fac, S, info);
   return cudaGetLastError();
 }
@@ -569,7 +593,8 @@ cudaError_t chp1d_coarse_sweep(const chp_grid& g, const chp_spec& sp, int mode, 
                                double* tmp, chp_sys_info* info, cudaStream_t st) {
   Scratch1 S{ub, yh, tmp, nic};
   const int bs = 32;
-  k1d_coarse_sweep<<<(nic + bs - 1) / bs, bs, 0, st>>>(g, sp, mode, nic, nsl, n0, n1, U, F, G,
+  const int smem = sp.scheme == CHP_LINEAR_B ? 0 : kRingBytes;
+  k1d_coarse_sweep<<<(nic + bs - 1) / bs, bs, smem, st>>>(g, sp, mode, nic, nsl, n0, n1, U, F, G,
                                                        ic_stride, sl_stride, changed, inc, fac,
                                                        S, info);
   return cudaGetLastError();
