@@ -38,8 +38,9 @@ typedef enum {
   CHP_ERR_UNSUPPORTED = 3   /* grid/scheme combination not implemented */
 } chp_status;
 
-/* Scheme ids -- reference schemes.py:52-58 (NN_LINEAR_A is out of scope). */
-enum { CHP_LINEAR_A = 0, CHP_LINEAR_B = 1, CHP_NONLINEAR_EYRE = 2 };
+/* Scheme ids -- reference schemes.py:52-58.  NN_LINEAR_A (ddm.py) has its own
+ * entry point, chp_nn_propagate, because it carries NN parameters. */
+enum { CHP_LINEAR_A = 0, CHP_LINEAR_B = 1, CHP_NONLINEAR_EYRE = 2, CHP_NN_LINEAR_A = 3 };
 
 /* Per-system outcome codes. */
 enum {
@@ -47,7 +48,10 @@ enum {
   CHP_SYS_NEWTON = 1,     /* NewtonDivergenceError (schemes.py:301-302)      */
   CHP_SYS_NONFINITE = 2,  /* ValueError non-finite field (grid.py:84-85)     */
   CHP_SYS_SINGULAR = 3,   /* zero pivot / not SPD (LinearSolveError)          */
-  CHP_SYS_CG = 4          /* 2D CG budget exhausted (LinearSolveError)        */
+  CHP_SYS_CG = 4,         /* 2D CG budget exhausted (LinearSolveError)        */
+  CHP_SYS_NN = 5          /* NNConvergenceError (ddm.py:331-332): fail_iter =
+                             sweeps, fail_resid = u-trace increment,
+                             newton_maxres = v-trace increment               */
 };
 
 /* Spatial grid (grid.py:33-67, operator coefficients of grid.py:98-118). */
@@ -150,6 +154,37 @@ chp_status chp_max_abs_diff(chp_ctx* ctx, const chp_grid* g, int n_fields,
                             const double* a, long long a_stride,
                             const double* b, long long b_stride,
                             double* out, void* stream);
+
+/* Neumann-Neumann interface-iteration parameters (ddm.py:51-66, NNParams)
+ * plus h**2 formed by the caller as grid.h**2 (ddm.py:274). */
+typedef struct {
+  int n_subdomains;   /* >= 2, divides nx - 1, (nx-1)/n >= 2; <= 32 here */
+  int max_iter;       /* sweep budget */
+  int warm_start;     /* carry the traces from step to step (ddm.py:367-371) */
+  int pad_;
+  double theta;       /* relaxation in (0, 1) */
+  double tol;         /* stop when both trace increments <= tol */
+  double h2;          /* grid.h**2 */
+} chp_nn_params;
+
+/*
+ * chp_nn_propagate -- `steps` Neumann-Neumann steps (Scheme.NN_LINEAR_A) on
+ * `nsys` 1D fields.  Replaces ddm.nn_propagate (ddm.py:360-372), hence
+ * schemes.propagate's NN_LINEAR_A branch (schemes.py:326-329); with steps = 1
+ * and traces it is ddm._nn_solve (ddm.py:268-340).  eps2 = eps**2 formed by
+ * the caller (ddm.py:275).  Fields/strides/sys_index/info as chp_propagate.
+ * traces_in (optional, device, nsys' x 2 x (n-1) doubles indexed by idx(s):
+ * g then h) seeds the first step's traces (zeros when NULL); traces_out
+ * (optional) receives the final step's converged traces.  info: newton_steps
+ * += steps, newton_total += interface sweeps, newton_max = max sweeps per
+ * step, newton_maxres = max accepted trace increment.
+ */
+chp_status chp_nn_propagate(chp_ctx* ctx, const chp_grid* g, const chp_nn_params* nn,
+                            double dt, double eps2, int steps, int nsys,
+                            const double* in, long long in_stride,
+                            double* out, long long out_stride, const int* sys_index,
+                            const double* traces_in, double* traces_out,
+                            chp_sys_info* info, void* stream);
 
 /* Debug: barrier timestamps (globaltimer ns) of the last cooperative 2D
  * coarse sweep when CHP_COOP_TRACE is set in the environment; returns the

@@ -333,6 +333,7 @@ class Knobs:
     pcg: bool = False          # 2D variable-coefficient solves by DST-preconditioned CG
     newton_tol: float = 1e-10
     newton_max_iter: int = 50
+    nn: object = None          # NNSetup: the fine propagator is NN_LINEAR_A (parareal.py:111-125)
 
 
 @dataclass
@@ -413,6 +414,158 @@ def advance(mesh, v, scheme, dt, eps, steps, knobs: Knobs, counter=None):
 
 
 # ----------------------------------------------------------------------------
+# Neumann-Neumann fine step (ddm.py) -- Scheme.NN_LINEAR_A, 1D only
+# ----------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class NNSetup:
+    """ddm.py:51-66 (NNParams)."""
+    n_subdomains: int = 8
+    theta: float = 0.25
+    tol: float = 1e-10
+    max_iter: int = 100
+    warm_start: bool = False
+
+
+class NNFailure(RuntimeError):
+    """ddm.py:121-133 (NNConvergenceError): sweeps, g/h increments."""
+
+    def __init__(self, sweeps, g_inc, h_inc):
+        super().__init__(f"NN did not converge in {sweeps} sweeps: {g_inc:.3e}, {h_inc:.3e}")
+        self.sweeps, self.g_inc, self.h_inc = sweeps, g_inc, h_inc
+
+
+def _mixed_block(k: int, hh: float, dt: float, eps2: float, c2: np.ndarray) -> np.ndarray:
+    """The 2k x 2k mixed (u, v) matrix [[I, -dt*Lap], [eps2*Lap - diag(c2), I]]
+    with the dense tridiagonal Lap = (1/h^2) tridiag(1, -2, 1) (ddm.py:136-142,
+    167-173, 211-217)."""
+    lap = np.zeros((k, k))
+    r = np.arange(k)
+    lap[r, r] = -2.0 / hh
+    lap[r[:-1], r[:-1] + 1] = 1.0 / hh
+    lap[r[1:], r[1:] - 1] = 1.0 / hh
+    A = np.zeros((2 * k, 2 * k))
+    A[:k, :k] = np.eye(k)
+    A[:k, k:] = -dt * lap
+    A[k:, :k] = eps2 * lap - np.diag(c2)
+    A[k:, k:] = np.eye(k)
+    return A
+
+
+def nn_subdomain(nodes: int, i: int, n_sub: int, uf: np.ndarray, hh: float, dt: float,
+                 eps2: float):
+    """Dirichlet solution at zero traces + its trace responses, and the Neumann
+    interface responses, of subdomain i (ddm.py:147-256).  ``uf``: the field
+    with its two boundary zeros (nodes entries); dense LAPACK LU (getrf/getrs
+    through scipy.linalg.lu_factor / lu_solve) exactly as the reference."""
+    step = (nodes - 1) // n_sub
+    a, b = i * step, (i + 1) * step
+    c2f = uf * uf
+    k = b - a - 1
+    Ad = _mixed_block(k, hh, dt, eps2, c2f[a + 1:b])
+    R = np.zeros((2 * k, 5))
+    R[:k, 0] = uf[a + 1:b]
+    R[k:, 0] = -uf[a + 1:b]
+    R[k, 1] = -eps2 / hh
+    R[0, 2] = dt / hh
+    R[2 * k - 1, 3] = -eps2 / hh
+    R[k - 1, 4] = dt / hh
+    X = sla.lu_solve(sla.lu_factor(Ad, check_finite=False), R, check_finite=False)
+    ends = [0, k - 1, k, 2 * k - 1]
+    lo_if, hi_if = a > 0, b < nodes - 1
+    an = a if lo_if else a + 1
+    bn = b if hi_if else b - 1
+    kn = bn - an + 1
+    c2n = c2f[an:bn + 1]
+    An = _mixed_block(kn, hh, dt, eps2, c2n)
+    for side, p, q in ((lo_if, 0, 1), (hi_if, kn - 1, kn - 2)):
+        if not side:
+            continue
+        # half-stencil interface rows (ddm.py:218-236)
+        An[p, :] = 0.0
+        An[p, p] = 0.5
+        An[p, kn + p] = dt / hh
+        An[p, kn + q] = -dt / hh
+        An[kn + p, :] = 0.0
+        An[kn + p, p] = -eps2 / hh - 0.5 * c2n[p]
+        An[kn + p, q] = eps2 / hh
+        An[kn + p, kn + p] = 0.5
+    loads = np.zeros((2 * kn, 4))
+    if lo_if:
+        loads[0, 0] = 1.0
+        loads[kn, 1] = 1.0
+    if hi_if:
+        loads[kn - 1, 2] = 1.0
+        loads[2 * kn - 1, 3] = 1.0
+    Y = sla.lu_solve(sla.lu_factor(An, check_finite=False), loads, check_finite=False)
+    return dict(a=a, b=b, sol0=X[:, 0], resp=X[:, 1:], edge0=X[ends, 0],
+                edge_resp=X[ends, 1:], neu=Y[[0, kn - 1, kn, 2 * kn - 1], :])
+
+
+def nn_step(mesh: Mesh, v: np.ndarray, dt: float, eps: float, nn: NNSetup, g=None, h=None):
+    """ddm.py:259-340 (_nn_solve): relaxed interface iteration on the traces,
+    then assembly.  Returns (values, g, h, sweeps)."""
+    if mesh.dim != 1:
+        raise ValueError("domain decomposition is implemented in 1D only")
+    nodes, hh, eps2, S = mesh.nx, mesh.h ** 2, eps ** 2, nn.n_subdomains
+    step = (nodes - 1) // S
+    iface = np.arange(1, S) * step
+    uf = np.zeros(nodes)
+    uf[1:-1] = v
+    c2f = uf * uf
+    subs = [nn_subdomain(nodes, i, S, uf, hh, dt, eps2) for i in range(S)]
+    g = np.zeros(S - 1) if g is None else g.copy()
+    h = np.zeros(S - 1) if h is None else h.copy()
+
+    def traces(i):     # ddm.py:259-265
+        return np.array([g[i - 1] if i > 0 else 0.0, h[i - 1] if i > 0 else 0.0,
+                         g[i] if i < S - 1 else 0.0, h[i] if i < S - 1 else 0.0])
+
+    gi = hi = np.inf
+    for sweep in range(1, nn.max_iter + 1):
+        E = np.array([sd["edge0"] + sd["edge_resp"] @ traces(i) for i, sd in enumerate(subs)])
+        ju = g - dt * (E[:-1, 3] + E[1:, 2] - 2.0 * h) / hh - uf[iface]
+        jv = eps2 * (E[:-1, 1] + E[1:, 0] - 2.0 * g) / hh - c2f[iface] * g + h + uf[iface]
+        P = np.zeros((S, 4))
+        for i, sd in enumerate(subs):
+            ld = np.array([-ju[i - 1] if i > 0 else 0.0, -jv[i - 1] if i > 0 else 0.0,
+                           ju[i] if i < S - 1 else 0.0, jv[i] if i < S - 1 else 0.0])
+            P[i] = sd["neu"] @ ld
+        dg = nn.theta * (P[:-1, 1] - P[1:, 0])
+        dh = nn.theta * (P[:-1, 3] - P[1:, 2])
+        g -= dg
+        h -= dh
+        gi = math.sqrt(mesh.h * float(np.dot(dg, dg)))
+        hi = math.sqrt(mesh.h * float(np.dot(dh, dh)))
+        if gi <= nn.tol and hi <= nn.tol:
+            break
+    else:
+        raise NNFailure(nn.max_iter, gi, hi)
+    out = np.empty(mesh.size)
+    for i, sd in enumerate(subs):
+        sol = sd["sol0"] + sd["resp"] @ traces(i)
+        k = sd["b"] - sd["a"] - 1
+        out[sd["a"]:sd["b"] - 1] = sol[:k]
+    out[iface - 1] = g
+    return out, g, h, sweep
+
+
+def nn_advance(mesh: Mesh, v: np.ndarray, dt: float, eps: float, nn: NNSetup, steps: int,
+               sweeps: list | None = None):
+    """ddm.py:360-372 (nn_propagate): traces restart from zero each step unless
+    warm_start carries them over."""
+    g = h = None
+    for _ in range(steps):
+        v, g1, h1, sw = nn_step(mesh, v, dt, eps, nn, g, h)
+        v = check_finite(v)
+        if sweeps is not None:
+            sweeps.append(sw)
+        if nn.warm_start:
+            g, h = g1, h1
+    return v
+
+
+# ----------------------------------------------------------------------------
 # Parareal (parareal.py:145-374) with the increment stop of SURVEY.md 8(a) a20
 # ----------------------------------------------------------------------------
 
@@ -429,12 +582,20 @@ class PararealResult:
     seconds: float
 
 
+def fine_advance(mesh, v, fine, dt, eps, J, knobs: Knobs, counter=None):
+    """F: the variant's fine scheme, or the NN step when ``knobs.nn`` is set
+    (parareal.py:111-125 replaces the fine spec by Scheme.NN_LINEAR_A)."""
+    if knobs.nn is not None:
+        return nn_advance(mesh, v, dt, eps, knobs.nn, J)
+    return advance(mesh, v, fine, dt, eps, J, knobs, counter)
+
+
 def serial_fine(mesh, u0, variant, T, N, J, eps, knobs: Knobs, counter=None):
     """parareal.py:145-164."""
     fine = VARIANTS[variant][0]
     out = [u0]
     for _ in range(N):
-        out.append(advance(mesh, out[-1], fine, T / N / J, eps, J, knobs, counter))
+        out.append(fine_advance(mesh, out[-1], fine, T / N / J, eps, J, knobs, counter))
     return np.array(out)
 
 
@@ -478,7 +639,7 @@ def parareal(mesh, u0, variant, T, N, J, eps, knobs: Knobs | None = None, *,
     while k < max_iter:
         for n in range(N):
             if changed[n] or not skip_stable:
-                Fv[n] = advance(mesh, U[n], fine, dt, eps, J, knobs, counter)
+                Fv[n] = fine_advance(mesh, U[n], fine, dt, eps, J, knobs, counter)
                 fine_props += 1
         newU = U.copy()
         new_changed = np.zeros(N + 1, bool)

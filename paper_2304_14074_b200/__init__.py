@@ -8,4 +8,4 @@ sm_100a CUDA kernels in ``libchp.so`` (see ``include/chp.h``).
 
 __version__ = "0.1.0"
 
-from . import grid, schemes, parareal  # noqa: F401,E402
+from . import grid, schemes, parareal, ddm  # noqa: F401,E402

@@ -17,14 +17,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # CHP_LIB: alternative build of the same library (kernel-variant A/B timing only)
 LIB_PATH = os.environ.get("CHP_LIB") or os.path.join(_HERE, "libchp.so")
 
-CHP_LINEAR_A, CHP_LINEAR_B, CHP_NONLINEAR_EYRE = 0, 1, 2
-SYS_OK, SYS_NEWTON, SYS_NONFINITE, SYS_SINGULAR, SYS_CG = 0, 1, 2, 3, 4
+CHP_LINEAR_A, CHP_LINEAR_B, CHP_NONLINEAR_EYRE, CHP_NN_LINEAR_A = 0, 1, 2, 3
+SYS_OK, SYS_NEWTON, SYS_NONFINITE, SYS_SINGULAR, SYS_CG, SYS_NN = 0, 1, 2, 3, 4, 5
 
 # Exported symbols, one per declaration in include/chp.h.
 EXPORTS = (
     "chp_version", "chp_status_str", "chp_ctx_create", "chp_ctx_destroy", "chp_last_error",
     "chp_sysinfo_reset", "chp_propagate", "chp_coarse_sweep", "chp_max_abs_diff",
-    "chp_debug_trace",
+    "chp_debug_trace", "chp_nn_propagate",
 )
 
 
@@ -39,6 +39,12 @@ class ChpSpec(C.Structure):
     _fields_ = [("scheme", C.c_int), ("newton_max_iter", C.c_int), ("dt", C.c_double),
                 ("eps", C.c_double), ("b", C.c_double), ("newton_tol", C.c_double),
                 ("cg_tol", C.c_double), ("cg_max_iter", C.c_int), ("pad_", C.c_int)]
+
+
+class ChpNNParams(C.Structure):
+    _fields_ = [("n_subdomains", C.c_int), ("max_iter", C.c_int), ("warm_start", C.c_int),
+                ("pad_", C.c_int), ("theta", C.c_double), ("tol", C.c_double),
+                ("h2", C.c_double)]
 
 
 class ChpSysInfo(C.Structure):
@@ -81,6 +87,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                    vp, vp, vp, ll, ll, vp, vp, vp, vp]
     L.chp_max_abs_diff.argtypes = [vp, C.POINTER(ChpGrid), i, vp, ll, vp, ll, vp, vp]
     L.chp_debug_trace.argtypes = [vp, i]
+    L.chp_nn_propagate.argtypes = [vp, C.POINTER(ChpGrid), C.POINTER(ChpNNParams), d, d, i, i,
+                                   vp, ll, vp, ll, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("chp_version", "chp_status_str", "chp_last_error"):
             getattr(L, name).restype = C.c_int

@@ -24,6 +24,12 @@ cudaError_t chp1d_coarse_sweep(const chp_grid& g, const chp_spec& sp, int mode, 
 cudaError_t chp_launch_max_abs_diff(const chp_grid& g, int n_fields, const double* a,
                                     long long as, const double* b, long long bs, double* out,
                                     cudaStream_t st);
+size_t chp_nn_scratch_bytes(int step, int nsys, int S);
+cudaError_t chp_nn_launch(const chp_grid& gr, const chp_nn_params& p, double dt, double eps2,
+                          int steps, int nsys, const double* in, long long in_stride,
+                          double* out, long long out_stride, const int* sys_index,
+                          const double* traces_in, double* traces_out, chp_sys_info* info,
+                          double* scratch, cudaStream_t st);
 struct Chp2d;
 Chp2d* chp2d_create();
 void chp2d_destroy(Chp2d*);
@@ -253,6 +259,46 @@ chp_status chp_max_abs_diff(chp_ctx* c, const chp_grid* g, int n_fields, const d
   if (n_fields == 0) return CHP_OK;
   cudaError_t e = chp_launch_max_abs_diff(*g, n_fields, a, as, b, bs, out, (cudaStream_t)stream);
   return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "max_abs_diff");
+}
+
+chp_status chp_nn_propagate(chp_ctx* c, const chp_grid* g, const chp_nn_params* nn, double dt,
+                            double eps2, int steps, int nsys, const double* in,
+                            long long in_stride, double* out, long long out_stride,
+                            const int* sys_index, const double* traces_in, double* traces_out,
+                            chp_sys_info* info, void* stream) {
+  if (!c) return CHP_ERR_ARG;
+  std::string why;
+  if (!grid_ok(g, &why)) return fail(c, CHP_ERR_ARG, why);
+  if (!nn) return fail(c, CHP_ERR_ARG, "null nn params");
+  // Decomposition / NNParams validation (ddm.py:58-66, 77-93)
+  if (g->dim != 1) return fail(c, CHP_ERR_ARG, "domain decomposition is implemented in 1D only");
+  if (nn->n_subdomains < 2) return fail(c, CHP_ERR_ARG, "need at least 2 subdomains");
+  const int cells = g->nx - 1;
+  if (cells % nn->n_subdomains != 0) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "%d mesh cells do not split evenly into %d subdomains", cells,
+             nn->n_subdomains);
+    return fail(c, CHP_ERR_ARG, buf);
+  }
+  if (cells / nn->n_subdomains < 2)
+    return fail(c, CHP_ERR_ARG, "subdomains must span at least 2 mesh cells");
+  if (!(nn->theta > 0.0 && nn->theta < 1.0))
+    return fail(c, CHP_ERR_ARG, "theta must lie in (0, 1)");
+  if (!(nn->tol > 0.0) || nn->max_iter < 1)
+    return fail(c, CHP_ERR_ARG, "tol must be positive and max_iter at least 1");
+  if (nn->n_subdomains > 32)
+    return fail(c, CHP_ERR_UNSUPPORTED, "at most 32 subdomains (one warp per system)");
+  if (!(dt > 0.0) || !(nn->h2 > 0.0)) return fail(c, CHP_ERR_ARG, "dt and h2 must be positive");
+  if (steps < 1) return fail(c, CHP_ERR_ARG, "steps must be at least 1");
+  if (nsys < 0 || !in || !out || !info) return fail(c, CHP_ERR_ARG, "bad arrays");
+  if (nsys == 0) return CHP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int step = cells / nn->n_subdomains;
+  chp_status s = ensure_scratch(c, chp_nn_scratch_bytes(step, nsys, nn->n_subdomains), st);
+  if (s != CHP_OK) return s;
+  cudaError_t e = chp_nn_launch(*g, *nn, dt, eps2, steps, nsys, in, in_stride, out, out_stride,
+                                sys_index, traces_in, traces_out, info, c->scratch, st);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp_nn_propagate");
 }
 
 }  // extern "C"

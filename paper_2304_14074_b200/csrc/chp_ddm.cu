@@ -1,0 +1,403 @@
+// Neumann-Neumann fine step (Scheme.NN_LINEAR_A) on sm_100a -- the B200
+// restatement of the reference's ddm.py (1D only, as the reference).
+//
+// One time step (ddm.py:268-340, _nn_solve) on a field of `nodes` grid points
+// split into S subdomains of `step` cells sharing their end points:
+//   * per subdomain, the Dirichlet solve of the mixed (u, v) system with zero
+//     traces plus its response to the four local traces (ddm.py:147-203), and
+//     the Neumann solve's interface values per unit load (ddm.py:205-256);
+//   * the relaxed interface iteration on the traces g (u) and h (v)
+//     (ddm.py:293-330), stopping once both cell-weighted L2 increments are
+//     <= tol, or NNConvergenceError after max_iter sweeps (ddm.py:331-332);
+//   * assembly of u^{n+1} = Dirichlet solution at the converged traces, with
+//     the traces themselves at the interface nodes (ddm.py:334-340).
+//
+// Mapping: one warp segment of W = next_pow2(S) lanes per system, lane i =
+// subdomain i; 32/W systems per warp.  The interface iteration exchanges the
+// edge values and Neumann loads with the neighbouring subdomains by warp
+// shuffles inside the segment -- no shared or global memory in the sweep loop.
+//
+// The reference factors each 2k x 2k mixed matrix by dense LAPACK LU.  Here
+// the same matrix, ordered node by node as x_k = (u_k, v_k), is block
+// tridiagonal with 2x2 blocks and is solved by block elimination (x_k =
+// z_k - G_k x_{k+1}); G_k and z_k live in a per-lane global scratch column
+// (coalesced across the lanes of a warp).  Same system, different rounding:
+// parity against the oracle is by tolerance (tests/test_gpu_nn.py).
+#include <math.h>
+
+#include "chp_common.cuh"
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kRow = 10;  // scratch doubles per node: G (4) + z of three columns (6)
+
+struct NNConst {
+  double dt, eps2, hh, hgrid, theta, tol;
+  double au, av;    // regular couplings: u-row to v_{k+-1}, v-row to u_{k+-1}
+  double bu, bv0;   // regular diagonal block [[1, bu], [bv0 - c2, 1]]
+  double iu, iv0;   // Neumann interface diagonal [[0.5, iu], [iv0 - 0.5 c2, 0.5]]
+  double cu, cv;    // Neumann interface couplings
+  double rg, rh;    // Dirichlet trace loads: v-row (g), u-row (h)
+  int nodes, step, S, W, max_iter, warm, steps, nsys;
+};
+
+struct B2 {  // [[a, b], [c, d]]
+  double a, b, c, d;
+};
+
+CHP_DEV B2 inv2(const B2& m) {
+  const double r = 1.0 / (m.a * m.d - m.b * m.c);
+  return {m.d * r, -m.b * r, -m.c * r, m.a * r};
+}
+
+// Off-diagonal blocks are anti-diagonal: [[0, p], [q, 0]].
+// D - A*G with A = [[0,p],[q,0]]
+CHP_DEV B2 schur(const B2& D, double p, double q, const B2& G) {
+  return {D.a - p * G.c, D.b - p * G.d, D.c - q * G.a, D.d - q * G.b};
+}
+// Dinv * [[0,p],[q,0]]
+CHP_DEV B2 times_anti(const B2& Di, double p, double q) {
+  return {Di.b * q, Di.a * p, Di.d * q, Di.c * p};
+}
+
+struct Scratch {
+  double* base;
+  size_t nl;   // lanes in the launch (column stride)
+  size_t gl;   // this lane's column
+  CHP_DEV double& at(int k, int f) const { return base[((size_t)k * kRow + f) * nl + gl]; }
+};
+
+// Forward block elimination of one subdomain system; stores G_k and z_k of the
+// columns named by the caller.  `neu`: Neumann variant (interface half rows).
+// Dirichlet: K = step-1 nodes a+1..b-1, columns (un), (g_left), (h_left).
+// Neumann:   K = bn-an+1 nodes, columns (left u load), (left v load).
+// Returns the last pivot inverse (the right-end loads are applied at K-1 only).
+template <bool kNeu>
+CHP_DEV B2 eliminate(const NNConst& c, const Scratch& sc, const double* u,
+                     int first_node, int K, bool lo_if, bool hi_if) {
+  B2 G = {0, 0, 0, 0};
+  double z[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  B2 Di = {0, 0, 0, 0};
+  for (int k = 0; k < K; ++k) {
+    const int node = first_node + k;
+    const double un = u[node - 1];
+    const double c2 = un * un;
+    const bool iface = kNeu && ((k == 0 && lo_if) || (k == K - 1 && hi_if));
+    B2 D = iface ? B2{0.5, c.iu, c.iv0 - 0.5 * c2, 0.5} : B2{1.0, c.bu, c.bv0 - c2, 1.0};
+    // coupling to k-1 (A_k) and to k+1 (C_k)
+    const bool a_if = kNeu && (k == K - 1 && hi_if);
+    const bool c_if = kNeu && (k == 0 && lo_if);
+    const double ap = a_if ? c.cu : c.au, aq = a_if ? c.cv : c.av;
+    const double cp = c_if ? c.cu : c.au, cq = c_if ? c.cv : c.av;
+    double r[3][2];
+    if (kNeu) {
+      r[0][0] = (k == 0 && lo_if) ? 1.0 : 0.0; r[0][1] = 0.0;
+      r[1][0] = 0.0; r[1][1] = (k == 0 && lo_if) ? 1.0 : 0.0;
+      r[2][0] = r[2][1] = 0.0;
+    } else {
+      r[0][0] = un; r[0][1] = -un;
+      r[1][0] = 0.0; r[1][1] = k == 0 ? c.rg : 0.0;
+      r[2][0] = k == 0 ? c.rh : 0.0; r[2][1] = 0.0;
+    }
+    if (k > 0) {
+      D = schur(D, ap, aq, G);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        r[j][0] -= ap * z[j][1];
+        r[j][1] -= aq * z[j][0];
+      }
+    }
+    Di = inv2(D);
+    G = times_anti(Di, cp, cq);
+    const int ncol = kNeu ? 2 : 3;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (j >= ncol) break;
+      const double z0 = Di.a * r[j][0] + Di.b * r[j][1];
+      const double z1 = Di.c * r[j][0] + Di.d * r[j][1];
+      z[j][0] = z0;
+      z[j][1] = z1;
+      sc.at(k, 4 + 2 * j) = z0;
+      sc.at(k, 5 + 2 * j) = z1;
+    }
+    sc.at(k, 0) = G.a; sc.at(k, 1) = G.b; sc.at(k, 2) = G.c; sc.at(k, 3) = G.d;
+  }
+  return Di;
+}
+
+__global__ void __launch_bounds__(128) k_nn_propagate(
+    NNConst c, const double* in, long long in_stride, double* out,
+    long long out_stride, const int* __restrict__ sys_index, const double* traces_in,
+    double* traces_out, SysInfo* info, double* scratch) {
+  const int lane = threadIdx.x & 31;
+  const int W = c.W, S = c.S;
+  const int i = lane & (W - 1);            // subdomain
+  const int spw = 32 / W;
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long s = warp * spw + lane / W;   // system within the launch
+  const bool valid = s < c.nsys;
+  const bool lane_on = valid && i < S;
+  const int idx = valid ? (sys_index ? sys_index[s] : (int)s) : 0;
+  const Scratch sc{scratch, (size_t)gridDim.x * blockDim.x,
+                   (size_t)(blockIdx.x * blockDim.x + threadIdx.x)};
+  const int step = c.step;
+  const int a = i * step, b = (i + 1) * step;
+  const bool lo_if = a > 0, hi_if = i < S - 1;
+  const bool owns_if = lane_on && hi_if;   // lane i owns interface i (node b)
+
+  SysInfo* si = valid ? info + idx : nullptr;
+  bool live = valid && si->status == CHP_SYS_OK;
+  double g = 0.0, h = 0.0;
+  if (owns_if && traces_in) {
+    g = traces_in[(size_t)idx * 2 * (S - 1) + i];
+    h = traces_in[(size_t)idx * 2 * (S - 1) + (S - 1) + i];
+  }
+  long long sweeps_total = 0;
+  int sweeps_max = 0;
+  double res_max = 0.0;
+  int steps_done = 0;
+
+  for (int st = 0; st < c.steps; ++st) {
+    const double* u = st == 0 ? in + (size_t)idx * in_stride : out + (size_t)idx * out_stride;
+    double* o = out + (size_t)idx * out_stride;
+    if (st > 0 && !c.warm) g = h = 0.0;
+
+    // ---- Neumann interface responses (ddm.py:205-256) ----
+    double ner[4][4] = {};   // rows (phi_L, phi_R, psi_L, psi_R), cols (L_u, L_v, R_u, R_v)
+    double edge0[4] = {}, er[4][4] = {};  // rows (u_first, u_last, v_first, v_last)
+    double unode = 0.0, c2node = 0.0;
+    double zr[2][2] = {};    // Dirichlet right-end columns at K-1 (g_right, h_right)
+    if (lane_on && live) {
+      const int an = lo_if ? a : a + 1, bn = hi_if ? b : b - 1;
+      const int Kn = bn - an + 1;
+      const B2 Di = eliminate<true>(c, sc, u, an, Kn, lo_if, hi_if);
+      // columns 2,3 (right loads) are zero except at K-1: z_{K-1} = Di * e
+      double x[4][2];
+      x[0][0] = sc.at(Kn - 1, 4); x[0][1] = sc.at(Kn - 1, 5);
+      x[1][0] = sc.at(Kn - 1, 6); x[1][1] = sc.at(Kn - 1, 7);
+      x[2][0] = hi_if ? Di.a : 0.0; x[2][1] = hi_if ? Di.c : 0.0;
+      x[3][0] = hi_if ? Di.b : 0.0; x[3][1] = hi_if ? Di.d : 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { ner[1][j] = x[j][0]; ner[3][j] = x[j][1]; }
+      for (int k = Kn - 2; k >= 0; --k) {
+        const double Ga = sc.at(k, 0), Gb = sc.at(k, 1), Gc = sc.at(k, 2), Gd = sc.at(k, 3);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double z0 = j < 2 ? sc.at(k, 4 + 2 * j) : 0.0;
+          const double z1 = j < 2 ? sc.at(k, 5 + 2 * j) : 0.0;
+          const double x0 = z0 - (Ga * x[j][0] + Gb * x[j][1]);
+          const double x1 = z1 - (Gc * x[j][0] + Gd * x[j][1]);
+          x[j][0] = x0;
+          x[j][1] = x1;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { ner[0][j] = x[j][0]; ner[2][j] = x[j][1]; }
+
+      // ---- Dirichlet solution and trace responses (ddm.py:147-203) ----
+      const int K = step - 1;
+      const B2 Dd = eliminate<false>(c, sc, u, a + 1, K, false, false);
+      zr[0][0] = Dd.b * c.rg; zr[0][1] = Dd.d * c.rg;   // g_right: v-row load
+      zr[1][0] = Dd.a * c.rh; zr[1][1] = Dd.c * c.rh;   // h_right: u-row load
+      double y[5][2];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) { y[j][0] = sc.at(K - 1, 4 + 2 * j); y[j][1] = sc.at(K - 1, 5 + 2 * j); }
+      y[3][0] = zr[0][0]; y[3][1] = zr[0][1];
+      y[4][0] = zr[1][0]; y[4][1] = zr[1][1];
+      edge0[1] = y[0][0]; edge0[3] = y[0][1];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { er[1][j] = y[j + 1][0]; er[3][j] = y[j + 1][1]; }
+      for (int k = K - 2; k >= 0; --k) {
+        const double Ga = sc.at(k, 0), Gb = sc.at(k, 1), Gc = sc.at(k, 2), Gd = sc.at(k, 3);
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          const double z0 = j < 3 ? sc.at(k, 4 + 2 * j) : 0.0;
+          const double z1 = j < 3 ? sc.at(k, 5 + 2 * j) : 0.0;
+          const double x0 = z0 - (Ga * y[j][0] + Gb * y[j][1]);
+          const double x1 = z1 - (Gc * y[j][0] + Gd * y[j][1]);
+          y[j][0] = x0;
+          y[j][1] = x1;
+        }
+      }
+      edge0[0] = y[0][0]; edge0[2] = y[0][1];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { er[0][j] = y[j + 1][0]; er[2][j] = y[j + 1][1]; }
+      if (hi_if) {
+        unode = u[b - 1];
+        c2node = unode * unode;
+      }
+    }
+    __syncwarp();
+
+    // ---- interface iteration (ddm.py:293-332) ----
+    bool done = !live;
+    int sweep = 0;
+    double gi = INFINITY, hi = INFINITY;
+    while (__any_sync(kFull, !done)) {
+      if (!done) ++sweep;   // other segments of the warp may still be sweeping
+      const double gL0 = __shfl_up_sync(kFull, g, 1, W), hL0 = __shfl_up_sync(kFull, h, 1, W);
+      const double tr[4] = {i > 0 ? gL0 : 0.0, i > 0 ? hL0 : 0.0, hi_if ? g : 0.0,
+                            hi_if ? h : 0.0};
+      double e[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        e[r] = edge0[r] + (er[r][0] * tr[0] + er[r][1] * tr[1] + er[r][2] * tr[2] +
+                           er[r][3] * tr[3]);
+      const double uf_next = __shfl_down_sync(kFull, e[0], 1, W);
+      const double vf_next = __shfl_down_sync(kFull, e[2], 1, W);
+      double ju = 0.0, jv = 0.0;
+      if (owns_if) {
+        ju = g - c.dt * (e[3] + vf_next - 2.0 * h) / c.hh - unode;
+        jv = c.eps2 * (e[1] + uf_next - 2.0 * g) / c.hh - c2node * g + h + unode;
+      }
+      const double juL = __shfl_up_sync(kFull, ju, 1, W), jvL = __shfl_up_sync(kFull, jv, 1, W);
+      const double ld[4] = {i > 0 ? -juL : 0.0, i > 0 ? -jvL : 0.0, hi_if ? ju : 0.0,
+                            hi_if ? jv : 0.0};
+      double p[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        p[r] = ner[r][0] * ld[0] + ner[r][1] * ld[1] + ner[r][2] * ld[2] + ner[r][3] * ld[3];
+      const double phiL_next = __shfl_down_sync(kFull, p[0], 1, W);
+      const double psiL_next = __shfl_down_sync(kFull, p[2], 1, W);
+      double dg = 0.0, dh = 0.0;
+      if (owns_if && !done) {
+        dg = c.theta * (p[1] - phiL_next);
+        dh = c.theta * (p[3] - psiL_next);
+        g -= dg;
+        h -= dh;
+      }
+      double sg = dg * dg, sh = dh * dh;
+      for (int off = W >> 1; off > 0; off >>= 1) {
+        sg += __shfl_xor_sync(kFull, sg, off, W);
+        sh += __shfl_xor_sync(kFull, sh, off, W);
+      }
+      if (!done) {
+        gi = sqrt(c.hgrid * sg);
+        hi = sqrt(c.hgrid * sh);
+        if (gi <= c.tol && hi <= c.tol) {
+          done = true;
+        } else if (sweep >= c.max_iter) {
+          done = true;
+          live = false;
+          if (i == 0) {
+            sysinfo_fail(si, CHP_SYS_NN, c.max_iter, gi);
+            si->newton_maxres = hi;   // h increment of the failed step (chp.h)
+          }
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- assembly (ddm.py:334-340) ----
+    // left neighbour's traces (all lanes participate)
+    const double gLa = __shfl_up_sync(kFull, g, 1, W), hLa = __shfl_up_sync(kFull, h, 1, W);
+    if (lane_on && live) {
+      const double tg = i > 0 ? gLa : 0.0, th = i > 0 ? hLa : 0.0;
+      const double rgv = hi_if ? g : 0.0, rhv = hi_if ? h : 0.0;
+      const int K = step - 1;
+      bool fin = true;
+      double x0 = sc.at(K - 1, 4) + (tg * sc.at(K - 1, 6) + th * sc.at(K - 1, 8) +
+                                     rgv * zr[0][0] + rhv * zr[1][0]);
+      double x1 = sc.at(K - 1, 5) + (tg * sc.at(K - 1, 7) + th * sc.at(K - 1, 9) +
+                                     rgv * zr[0][1] + rhv * zr[1][1]);
+      o[a + K - 1] = x0;
+      fin &= isfinite(x0);
+      for (int k = K - 2; k >= 0; --k) {
+        const double z0 = sc.at(k, 4) + (tg * sc.at(k, 6) + th * sc.at(k, 8));
+        const double z1 = sc.at(k, 5) + (tg * sc.at(k, 7) + th * sc.at(k, 9));
+        const double n0 = z0 - (sc.at(k, 0) * x0 + sc.at(k, 1) * x1);
+        const double n1 = z1 - (sc.at(k, 2) * x0 + sc.at(k, 3) * x1);
+        x0 = n0;
+        x1 = n1;
+        o[a + k] = x0;
+        fin &= isfinite(x0);
+      }
+      if (hi_if) {
+        o[b - 1] = g;
+        fin &= isfinite(g);
+      }
+      if (!fin) {
+        sysinfo_fail(si, CHP_SYS_NONFINITE, st + 1, 0.0);
+      }
+      if (i == 0) {
+        sweeps_total += sweep;
+        sweeps_max = max(sweeps_max, sweep);
+        res_max = fmax(res_max, fmax(gi, hi));
+        ++steps_done;
+      }
+    }
+    __syncwarp();
+    // a non-finite lane stops its whole system (segment-uniform)
+    if (valid) {
+      const unsigned seg = __ballot_sync(kFull, lane_on && si->status != CHP_SYS_OK);
+      const unsigned mine = (W == 32 ? kFull : ((1u << W) - 1u)) << ((lane / W) * W);
+      if (seg & mine) live = false;
+    } else {
+      __ballot_sync(kFull, false);
+    }
+  }
+  if (lane_on && i < S - 1 && traces_out) {
+    traces_out[(size_t)idx * 2 * (S - 1) + i] = g;
+    traces_out[(size_t)idx * 2 * (S - 1) + (S - 1) + i] = h;
+  }
+  if (valid && i == 0 && steps_done > 0) {
+    si->newton_steps += steps_done;
+    si->newton_total += sweeps_total;
+    si->newton_max = max(si->newton_max, sweeps_max);
+    si->newton_maxres = fmax(si->newton_maxres, res_max);
+  }
+}
+
+}  // namespace
+
+size_t chp_nn_scratch_bytes(int step, int nsys, int S) {
+  int W = 1;
+  while (W < S) W <<= 1;
+  const int spw = 32 / W;
+  const long long warps = (nsys + spw - 1) / spw;
+  const long long blocks = (warps + 3) / 4;
+  return (size_t)(step + 1) * kRow * (size_t)(blocks * 128) * sizeof(double);
+}
+
+cudaError_t chp_nn_launch(const chp_grid& gr, const chp_nn_params& p, double dt, double eps2,
+                          int steps, int nsys, const double* in, long long in_stride,
+                          double* out, long long out_stride, const int* sys_index,
+                          const double* traces_in, double* traces_out, chp_sys_info* info,
+                          double* scratch, cudaStream_t st) {
+  NNConst c;
+  const double hh = p.h2;
+  c.dt = dt;
+  c.eps2 = eps2;
+  c.hh = hh;
+  c.hgrid = gr.h;
+  c.theta = p.theta;
+  c.tol = p.tol;
+  c.au = -dt * (1.0 / hh);
+  c.av = eps2 * (1.0 / hh);
+  c.bu = -dt * (-2.0 / hh);
+  c.bv0 = eps2 * (-2.0 / hh);
+  c.iu = dt / hh;
+  c.iv0 = -eps2 / hh;
+  c.cu = -dt / hh;
+  c.cv = eps2 / hh;
+  c.rg = -eps2 / hh;
+  c.rh = dt / hh;
+  c.nodes = gr.nx;
+  c.S = p.n_subdomains;
+  c.step = (gr.nx - 1) / p.n_subdomains;
+  int W = 1;
+  while (W < c.S) W <<= 1;
+  c.W = W;
+  c.max_iter = p.max_iter;
+  c.warm = p.warm_start;
+  c.steps = steps;
+  c.nsys = nsys;
+  const int spw = 32 / W;
+  const long long warps = (nsys + spw - 1) / spw;
+  const long long blocks = (warps + 3) / 4;
+  k_nn_propagate<<<(unsigned)blocks, 128, 0, st>>>(c, in, in_stride, out, out_stride, sys_index,
+                                                   traces_in, traces_out,
+                                                   reinterpret_cast<SysInfo*>(info), scratch);
+  return cudaGetLastError();
+}

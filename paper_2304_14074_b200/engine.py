@@ -50,8 +50,8 @@ class PararealEngine:
                  num_slices: int, fine_steps: int, batch: int = 1, device=None,
                  inc_tol: float = 1e-10, timing: bool = False):
         import torch
-        if fine.scheme is Scheme.NN_LINEAR_A or coarse.scheme is Scheme.NN_LINEAR_A:
-            raise NotImplementedError("NN_LINEAR_A is outside the B200 hot path")
+        if coarse.scheme is Scheme.NN_LINEAR_A:
+            raise ValueError("the coarse propagator cannot be NN_LINEAR_A (parareal.py:111-125)")
         self.grid, self.fine, self.coarse = grid, fine, coarse
         self.N, self.J, self.B = int(num_slices), int(fine_steps), int(batch)
         self.device = torch.device(device) if device is not None else torch.device(

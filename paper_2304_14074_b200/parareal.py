@@ -201,7 +201,8 @@ def parareal_iteration(state: PararealState, variant: AlgorithmVariant,
     eng = state._engine
     fresh = (eng is not None and eng.k == state.k and eng.N == Nsl
              and eng.J == partition.fine_steps and eng.fine.dt == partition.fine_dt
-             and eng.fine.eps == eps and eng.fine.scheme is variant.fine_scheme
+             and eng.fine.eps == eps and eng.fine.nn == nn
+             and eng.fine.scheme is (Scheme.NN_LINEAR_A if nn is not None else variant.fine_scheme)
              and eng.coarse.scheme is variant.coarse_scheme
              and eng.fine.newton_tol == newton_tol)
     if not fresh:

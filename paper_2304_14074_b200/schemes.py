@@ -86,8 +86,7 @@ class PropagatorSpec:
 
     def native(self):
         if self.scheme is Scheme.NN_LINEAR_A:
-            raise NotImplementedError(
-                "NN_LINEAR_A (ddm.py Neumann-Neumann) is outside the B200 hot path")
+            raise ValueError("NN_LINEAR_A launches through chp_nn_propagate (ddm.py)")
         return N.ChpSpec(_NATIVE_SCHEME[self.scheme], int(self.newton_max_iter), float(self.dt),
                          float(self.eps), self.eps ** 2 * self.dt, float(self.newton_tol),
                          CG_TOL, CG_MAX_ITER, 0)
@@ -186,6 +185,9 @@ def raise_on_status(info: np.ndarray, spec: PropagatorSpec, labels=None) -> None
         raise LinearSolveError("direct solve failed (singular pivot)" + where)
     if code == N.SYS_CG:
         raise LinearSolveError("CG did not reach the relative residual target" + where)
+    if code == N.SYS_NN:
+        from .ddm import _raise_nn
+        _raise_nn(info[s], spec.nn, where)
     raise RuntimeError(f"unknown device status {code}{where}")
 
 
@@ -200,6 +202,10 @@ def propagate_batch(grid: SpatialGrid, spec: PropagatorSpec, steps: int, src, ou
     """
     if steps < 1:
         raise ValueError(f"steps must be at least 1, got {steps}")
+    if spec.scheme is Scheme.NN_LINEAR_A:        # schemes.py:326-329 -> ddm
+        from .ddm import nn_propagate_batch
+        return nn_propagate_batch(grid, spec.nn, spec.dt, spec.eps, steps, src, out,
+                                  sys_index=sys_index, info=info, stream=stream, ctx=ctx)
     ctx = ctx or N.Context.get(src.device.index)
     fs = grid.device_size
     nfields = src.numel() // fs
@@ -266,9 +272,9 @@ def propagate(u: Field, spec: PropagatorSpec, steps: int,
     """Compose ``steps`` single steps (schemes.py:321-333) -- one launch."""
     if steps < 1:
         raise ValueError(f"steps must be at least 1, got {steps}")
-    if spec.scheme is Scheme.NN_LINEAR_A:
-        raise NotImplementedError(
-            "NN_LINEAR_A (ddm.py Neumann-Neumann) is outside the B200 hot path")
+    if spec.scheme is Scheme.NN_LINEAR_A:        # schemes.py:326-329
+        from .ddm import nn_propagate
+        return nn_propagate(u, spec, steps)
     out, si = _run_one(u, spec, steps)
     if stats is not None and spec.scheme is Scheme.NONLINEAR_EYRE:
         stats.absorb(si)
