@@ -155,6 +155,16 @@ chp_status chp_max_abs_diff(chp_ctx* ctx, const chp_grid* g, int n_fields,
                             const double* b, long long b_stride,
                             double* out, void* stream);
 
+/*
+ * chp_newton_history -- register (hist != NULL) or clear (NULL) a caller-owned
+ * device buffer that receives StepReport.residual_history (schemes.py:285-290):
+ * for every system idx(s) advanced by a later NONLINEAR_EYRE chp_propagate on
+ * this context, hist[idx * hist_len + it] = the residual norm before Newton
+ * solve `it` (it < hist_len) of its last step; entries after the accepted (or
+ * failing) iteration are left untouched.  Not used by chp_coarse_sweep.
+ */
+chp_status chp_newton_history(chp_ctx* ctx, double* hist, int hist_len);
+
 /* Neumann-Neumann interface-iteration parameters (ddm.py:51-66, NNParams)
  * plus h**2 formed by the caller as grid.h**2 (ddm.py:274). */
 typedef struct {

@@ -334,7 +334,7 @@ CHP_DEV bool step_linear_b(const G1& g, double dt, const double* __restrict__ fa
 // iteration count and residual (StepReport fields, schemes.py:291-300).
 CHP_DEV int step_eyre(const G1& g, double d, double b, double tol, int maxit,
                       const double* src, double* dst, double* yh, double* ub, long long ks,
-                      int* iters, double* res) {
+                      int* iters, double* res, double* hist, int hlen) {
   const int m = g.m;
   #pragma unroll 8
   for (int i = 0; i < m; ++i) {
@@ -365,6 +365,7 @@ CHP_DEV int step_eyre(const G1& g, double d, double b, double tol, int maxit,
       }
     }
     const double r = sqrt(g.hd * ss);
+    if (hist != nullptr && it < hlen) hist[it] = r;   // StepReport.residual_history
     if (r <= tol) {
       *iters = it;
       *res = r;
@@ -398,11 +399,14 @@ struct Scratch1 {   // per-launch interleaved scratch
   double* yh;       // [m][nthreads]
   double* tmp;      // [m][nthreads] (coarse sweep: g)
   long long ks;     // nthreads
+  double* hist;     // Newton residual history [nsys'][hlen] (chp_newton_history) or null
+  int hlen;
 };
 
 // One step of `scheme` for thread t.  Returns CHP_SYS_* and updates info.
 CHP_DEV int one_step(const G1& g, const chp_spec& sp, const double* fac, const double* src,
-                     double* dst, const Scratch1& S, int t, SysInfo* info) {
+                     double* dst, const Scratch1& S, int t, SysInfo* info,
+                     double* hist = nullptr) {
   int st = CHP_SYS_OK;
   double* ub = S.ub + t;
   double* yh = S.yh + t;
@@ -416,7 +420,7 @@ CHP_DEV int one_step(const G1& g, const chp_spec& sp, const double* fac, const d
     int it = 0;
     double r = 0.0;
     st = step_eyre(g, sp.dt, sp.b, sp.newton_tol, sp.newton_max_iter, src, dst, yh, ub, S.ks,
-                   &it, &r);
+                   &it, &r, hist, S.hlen);
     if (st == CHP_SYS_OK) {
       info->newton_steps += 1;
       info->newton_total += it;
@@ -493,7 +497,9 @@ __global__ void k1d_propagate(chp_grid gg, chp_spec sp, int steps, int nsys,
   SysInfo loc = *info;
   if (loc.status == CHP_SYS_OK) {
     for (int s = 0; s < steps; ++s) {
-      if (one_step(g, sp, fac, (s == 0) ? src : dst, dst, S, t, &loc) != CHP_SYS_OK) break;
+      if (one_step(g, sp, fac, (s == 0) ? src : dst, dst, S, t, &loc,
+                   S.hist ? S.hist + (long long)sidx * S.hlen : nullptr) != CHP_SYS_OK)
+        break;
     }
   }
   *info = loc;
@@ -577,8 +583,8 @@ cudaError_t chp1d_propagate(const chp_grid& g, const chp_spec& sp, int steps, in
                             const double* in, long long in_stride, double* out,
                             long long out_stride, const int* sys_index, const double* fac,
                             double* ub, double* yh, double* tmp, chp_sys_info* info,
-                            cudaStream_t st) {
-  Scratch1 S{ub, yh, tmp, nsys};
+                            cudaStream_t st, double* hist, int hlen) {
+  Scratch1 S{ub, yh, tmp, nsys, hist, hlen};
   const int bs = 32;
   const int smem = sp.scheme == CHP_LINEAR_B ? 0 : kRingBytes;
   k1d_propagate<<<(nsys + bs - 1) / bs, bs, smem, st>>>(g, sp, steps, nsys, in, in_stride, out,

@@ -447,6 +447,16 @@ __global__ void k2d_clear_flag(unsigned char* changed, int nic, int nsl, int slo
   if (i < nic && !(changed[(long long)i * (nsl + 1)] & 2)) changed[(long long)i * (nsl + 1) + slot] = 0;
 }
 
+// StepReport.residual_history (schemes.py:285-290): residual norm of Newton
+// iteration `it` of every active system into hist[idx * hlen + it]
+__global__ void k2d_newton_hist(int nsys, const double* res, const int* act, const int* sys_index,
+                                double* hist, int hlen, int it) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nsys || !act[s] || it >= hlen) return;
+  const int idx = sys_index ? sys_index[s] : s;
+  hist[(long long)idx * hlen + it] = res[s];
+}
+
 // add host-side Newton aggregates into the device sysinfo records
 struct NewtonRec { long long steps, total; int maxit, status, fail_iter, pad; double maxres, fail_res; };
 __global__ void k2d_newton_commit(int nsys, const NewtonRec* rec, chp_sys_info* info,
@@ -483,6 +493,8 @@ struct Chp2d {
   struct DTab { int N; double a2dt, b; double* d; };
   std::vector<DTab> dtabs;        // LINEAR_B spectral divisors, one per (N, dt, eps)
   void* coarse = nullptr;         // v2 coarse-sweep workspace
+  double* hist = nullptr;         // Newton residual history (chp_newton_history), caller owned
+  int hlen = 0;
   size_t coarse_bytes = 0;
   void* pcg = nullptr;            // v2 batched PCG workspace
   size_t pcg_bytes = 0;
@@ -492,6 +504,11 @@ struct Chp2d {
 };
 
 Chp2d* chp2d_create() { return new Chp2d(); }
+
+void chp2d_set_history(Chp2d* c, double* hist, int hlen) {
+  c->hist = hist;
+  c->hlen = hlen;
+}
 
 void chp2d_destroy(Chp2d* c) {
   if (!c) return;
@@ -748,6 +765,9 @@ cudaError_t run_variable(Chp2d* cx, const chp_grid& g, const chp_spec& sp, int s
                                           W.partial);
       k2d_newton_norm<<<(nsys + 7) / 8, 256, 0, st>>>(nsys, W.partial + (long long)nsys * kPB * 2,
                                                       g.hd, W.res, W.act);
+      if (cx->hist != nullptr && it < cx->hlen)
+        k2d_newton_hist<<<sb, 128, 0, st>>>(nsys, W.res, W.act, sys_index, cx->hist, cx->hlen,
+                                            it);
       cudaMemcpyAsync(hres, W.res, sizeof(double) * nsys, cudaMemcpyDeviceToHost, st);
       if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
       bool any = false;

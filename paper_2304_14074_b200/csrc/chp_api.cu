@@ -15,7 +15,7 @@ cudaError_t chp1d_propagate(const chp_grid& g, const chp_spec& sp, int steps, in
                             const double* in, long long in_stride, double* out,
                             long long out_stride, const int* sys_index, const double* fac,
                             double* ub, double* yh, double* tmp, chp_sys_info* info,
-                            cudaStream_t st);
+                            cudaStream_t st, double* hist, int hlen);
 cudaError_t chp1d_coarse_sweep(const chp_grid& g, const chp_spec& sp, int mode, int nic, int nsl,
                                int n0, int n1, double* U, const double* F, double* G,
                                long long ic_stride, long long sl_stride, unsigned char* changed,
@@ -33,6 +33,7 @@ cudaError_t chp_nn_launch(const chp_grid& gr, const chp_nn_params& p, double dt,
 struct Chp2d;
 Chp2d* chp2d_create();
 void chp2d_destroy(Chp2d*);
+void chp2d_set_history(Chp2d*, double* hist, int hlen);
 cudaError_t chp2d_propagate(Chp2d* c, const chp_grid& g, const chp_spec& sp, int steps, int nsys,
                             const double* in, long long in_stride, double* out,
                             long long out_stride, const int* sys_index, chp_sys_info* info,
@@ -53,6 +54,8 @@ struct chp_ctx {
   size_t scratch_bytes = 0;
   int* dev_err = nullptr;
   Chp2d* d2 = nullptr;
+  double* hist = nullptr;   // chp_newton_history buffer (caller owned)
+  int hlen = 0;
 };
 
 namespace {
@@ -204,7 +207,7 @@ chp_status chp_propagate(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int 
     double* yh = ub + (size_t)g->m * 7 * nsys;
     double* tmp = yh + (size_t)g->m * nsys;
     cudaError_t e = chp1d_propagate(*g, *sp, steps, nsys, in, in_stride, out, out_stride,
-                                    sys_index, fac, ub, yh, tmp, info, st);
+                                    sys_index, fac, ub, yh, tmp, info, st, c->hist, c->hlen);
     return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp1d_propagate");
   }
   cudaError_t e = chp2d_propagate(c->d2, *g, *sp, steps, nsys, in, in_stride, out, out_stride,
@@ -299,6 +302,15 @@ chp_status chp_nn_propagate(chp_ctx* c, const chp_grid* g, const chp_nn_params* 
   cudaError_t e = chp_nn_launch(*g, *nn, dt, eps2, steps, nsys, in, in_stride, out, out_stride,
                                 sys_index, traces_in, traces_out, info, c->scratch, st);
   return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp_nn_propagate");
+}
+
+chp_status chp_newton_history(chp_ctx* c, double* hist, int hist_len) {
+  if (!c) return CHP_ERR_ARG;
+  if (hist && hist_len < 1) return fail(c, CHP_ERR_ARG, "hist_len must be at least 1");
+  c->hist = hist;
+  c->hlen = hist ? hist_len : 0;
+  chp2d_set_history(c->d2, c->hist, c->hlen);
+  return CHP_OK;
 }
 
 }  // extern "C"

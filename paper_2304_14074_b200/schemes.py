@@ -94,9 +94,7 @@ class PropagatorSpec:
 
 @dataclass(frozen=True)
 class StepReport:
-    """Diagnostics of a single implicit step (schemes.py:89-97).  The device
-    Newton loop keeps only the accepted residual, so ``residual_history`` holds
-    that one value."""
+    """Diagnostics of a single implicit step (schemes.py:89-97)."""
 
     newton_iterations: int
     residual_norm: float
@@ -259,12 +257,24 @@ def step_linear_b(u: Field, spec: PropagatorSpec) -> Field:
 
 
 def step_nonlinear(u: Field, spec: PropagatorSpec) -> tuple[Field, StepReport]:
-    """One fully implicit Eyre step solved by Newton (schemes.py:270-305)."""
+    """One fully implicit Eyre step solved by Newton (schemes.py:270-305); the
+    device records the residual norm of every Newton iteration
+    (``chp_newton_history``) for ``StepReport.residual_history``."""
+    import torch
     _require(spec, Scheme.NONLINEAR_EYRE)
-    out, si = _run_one(u, spec, 1)
+    src = u.device_values()
+    ctx = N.Context.get(src.device.index)
+    hlen = int(spec.newton_max_iter) + 1
+    hist = torch.full((hlen,), float("nan"), dtype=torch.float64, device=src.device)
+    _check_ctx(ctx, ctx.L.chp_newton_history(ctx.h, N.ptr(hist), hlen), "chp_newton_history")
+    try:
+        out, si = _run_one(u, spec, 1)
+    finally:
+        ctx.L.chp_newton_history(ctx.h, None, 0)
     it = int(si["newton_total"][0])
     res = float(si["newton_maxres"][0])
-    return out, StepReport(it, res, energy(u, spec.eps), energy(out, spec.eps), (res,))
+    history = tuple(float(x) for x in hist[: it + 1].cpu().numpy())
+    return out, StepReport(it, res, energy(u, spec.eps), energy(out, spec.eps), history)
 
 
 def propagate(u: Field, spec: PropagatorSpec, steps: int,

@@ -238,3 +238,24 @@ def test_run_batch_matches_single_runs(P):
         ref = O.parareal(O.Mesh(1, 129), u0s[b].values, "npa1", 0.01, 4, 16, 0.05, EXACT)
         assert res.converged_at[b] == ref.k
         assert np.array_equal(res.engine.iterates_host(b), ref.iterates)
+
+
+@pytest.mark.parametrize("name", ["d1", "d1b", "d2"])
+def test_step_nonlinear_residual_history(P, golden, name):
+    """StepReport.residual_history (schemes.py:285-290) recorded on the device
+    (chp_newton_history) vs the reference's own step_nonlinear: same length
+    (iteration count), every pre-convergence residual to 1e-8 relative plus
+    1e-14 of the initial residual (2D solves are CG to 1e-14, not SuperLU), the
+    accepted one below newton_tol."""
+    _, schemes, grid = P
+    z = golden("newton_hist.npz")
+    dim, nx, dt, eps = z[f"{name}/params"]
+    g = grid.SpatialGrid(int(dim), int(nx))
+    spec = schemes.PropagatorSpec(schemes.Scheme.NONLINEAR_EYRE, float(dt), float(eps))
+    out, rep = schemes.step_nonlinear(grid.Field(g, z[f"{name}/u0"]), spec)
+    ref = z[f"{name}/hist"]
+    h = np.array(rep.residual_history)
+    assert len(h) == len(ref) == rep.newton_iterations + 1
+    assert np.all(np.abs(h[:-1] - ref[:-1]) <= 1e-8 * ref[:-1] + 1e-14 * ref[0])
+    assert h[-1] <= spec.newton_tol and h[-1] == rep.residual_norm
+    assert rel(out.values, z[f"{name}/out"]) < 1e-10
