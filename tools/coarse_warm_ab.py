@@ -3,6 +3,9 @@ coarse init + K Parareal iterations with cold and warm CG starts; per-iteration
 coarse-sweep seconds, CG iterations, and the max difference of the iterates.
 
     python tools/coarse_warm_ab.py [K]
+
+Needs the (rejected, reverted) warm-start patch: PararealEngine(coarse_warm=...)
+and chp_coarse_warm_start are not in the tree; kept as the record of the A/B.
 """
 import json
 import os
