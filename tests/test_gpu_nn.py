@@ -179,3 +179,30 @@ def test_nn_parareal_vs_reference(M, golden):
     assert np.max(np.abs(np.array(incs) - ref)) < ATOL
     U = np.array([f.values for f in st.iterates])
     assert np.max(np.abs(U - z["pr/U"])) < ATOL
+
+
+def test_nn_parareal_config2_grid_vs_oracle(M):
+    """NPA1-style run at config 2's grid (1D m = 1023, eps = 0.03) with the NN
+    fine propagator (8 subdomains): truncated Parareal (N = 4 slices, J = 8)
+    against the oracle's dense-LU restatement -- same increments to 1e-9 and
+    the same iteration at which the 1e-10 increment test fires."""
+    ddm, grid, parareal, _ = M
+    nx, eps, T, N, J = 1025, 0.03, 2.0 ** -9, 4, 8
+    g = grid.SpatialGrid(1, nx)
+    u0 = np.random.default_rng(11).uniform(-0.05, 0.05, nx - 2)
+    nn = ddm.NNParams(n_subdomains=8)
+    part = parareal.TimePartition(T, N, J)
+    var = parareal.AlgorithmVariant.PA1
+    init = parareal.coarse_init(grid.Field(g, u0), var, part, eps)
+    st = parareal.PararealState(iterates=init, coarse_values=init[1:], fine_reference=[], k=0)
+    incs = []
+    while st.k < N + 2:
+        st = parareal.parareal_iteration(st, var, part, eps, nn=nn)
+        incs.append(parareal.iterate_increment(st))
+        if incs[-1] < 1e-10:
+            break
+    ref = O.parareal(O.Mesh(1, nx), u0, "pa1", T, N, J, eps, O.Knobs(nn=O.NNSetup(8)))
+    assert len(incs) == len(ref.increments) and ref.k == len(incs)
+    assert np.max(np.abs(np.array(incs) - np.array(ref.increments))) < ATOL
+    U = np.array([f.values for f in st.iterates])
+    assert np.max(np.abs(U - ref.iterates)) < ATOL
