@@ -19,10 +19,13 @@
 //
 // The reference factors each 2k x 2k mixed matrix by dense LAPACK LU.  Here
 // the same matrix, ordered node by node as x_k = (u_k, v_k), is block
-// tridiagonal with 2x2 blocks and is solved by block elimination (x_k =
-// z_k - G_k x_{k+1}); G_k and z_k live in a per-lane global scratch column
-// (coalesced across the lanes of a warp).  Same system, different rounding:
-// parity against the oracle is by tolerance (tests/test_gpu_nn.py).
+// tridiagonal with 2x2 blocks.  The interface iteration needs only the END
+// values of the Dirichlet/Neumann solutions (edge responses), which a forward
+// and a reverse block elimination deliver without storing anything; only the
+// final assembly solve keeps G_k, z_k (6 doubles per node) in a per-lane
+// global scratch column for its back substitution (x_k = z_k - G_k x_{k+1}).
+// Same system, different rounding: parity against the reference is by
+// tolerance (tests/test_gpu_nn.py; measured <= 2e-15).
 #include <math.h>
 
 #include "chp_common.cuh"
@@ -30,7 +33,7 @@
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kRow = 10;  // scratch doubles per node: G (4) + z of three columns (6)
+constexpr int kRow = 6;   // assembly scratch doubles per node: G (4) + z (2)
 
 struct NNConst {
   double dt, eps2, hh, hgrid, theta, tol;
@@ -68,62 +71,86 @@ struct Scratch {
   CHP_DEV double& at(int k, int f) const { return base[((size_t)k * kRow + f) * nl + gl]; }
 };
 
-// Forward block elimination of one subdomain system; stores G_k and z_k of the
-// columns named by the caller.  `neu`: Neumann variant (interface half rows).
-// Dirichlet: K = step-1 nodes a+1..b-1, columns (un), (g_left), (h_left).
-// Neumann:   K = bn-an+1 nodes, columns (left u load), (left v load).
-// Returns the last pivot inverse (the right-end loads are applied at K-1 only).
+// Block elimination of one subdomain system, nodes k = 0..K-1 (first_node +
+// k), in direction kDir (+1: from k = 0, -1: from k = K-1), carrying NC
+// right-hand-side columns; returns the solution at the LAST processed node for
+// every column (x_{K-1} forward, x_0 reverse) -- no storage.  Row k:
+//   A_k x_{k-1} + B_k x_k + C_k x_{k+1} = r_k,   A, C = [[0, p], [q, 0]].
+// Processing order j: D_j = B - P G_{j-1}, G_j = D_j^-1 Nx, z_j = D_j^-1
+// (r - P z_{j-1}), with P the coupling to the previously processed node and Nx
+// the coupling to the next one.  `kNeu`: Neumann rows (ddm.py:218-236).
 template <bool kNeu>
-CHP_DEV B2 eliminate(const NNConst& c, const Scratch& sc, const double* u,
-                     int first_node, int K, bool lo_if, bool hi_if) {
-  B2 G = {0, 0, 0, 0};
-  double z[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-  B2 Di = {0, 0, 0, 0};
-  for (int k = 0; k < K; ++k) {
-    const int node = first_node + k;
-    const double un = u[node - 1];
-    const double c2 = un * un;
-    const bool iface = kNeu && ((k == 0 && lo_if) || (k == K - 1 && hi_if));
-    B2 D = iface ? B2{0.5, c.iu, c.iv0 - 0.5 * c2, 0.5} : B2{1.0, c.bu, c.bv0 - c2, 1.0};
-    // coupling to k-1 (A_k) and to k+1 (C_k)
-    const bool a_if = kNeu && (k == K - 1 && hi_if);
-    const bool c_if = kNeu && (k == 0 && lo_if);
-    const double ap = a_if ? c.cu : c.au, aq = a_if ? c.cv : c.av;
-    const double cp = c_if ? c.cu : c.au, cq = c_if ? c.cv : c.av;
-    double r[3][2];
-    if (kNeu) {
-      r[0][0] = (k == 0 && lo_if) ? 1.0 : 0.0; r[0][1] = 0.0;
-      r[1][0] = 0.0; r[1][1] = (k == 0 && lo_if) ? 1.0 : 0.0;
-      r[2][0] = r[2][1] = 0.0;
-    } else {
-      r[0][0] = un; r[0][1] = -un;
-      r[1][0] = 0.0; r[1][1] = k == 0 ? c.rg : 0.0;
-      r[2][0] = k == 0 ? c.rh : 0.0; r[2][1] = 0.0;
-    }
-    if (k > 0) {
-      D = schur(D, ap, aq, G);
+struct NodeRow {   // diagonal block and couplings of row k
+  B2 D;
+  double ap, aq, cp, cq;
+};
+
+template <bool kNeu>
+CHP_DEV NodeRow<kNeu> node_row(const NNConst& c, double c2, int k, int K, bool lo_if,
+                               bool hi_if) {
+  NodeRow<kNeu> n;
+  const bool iface = kNeu && ((k == 0 && lo_if) || (k == K - 1 && hi_if));
+  n.D = iface ? B2{0.5, c.iu, c.iv0 - 0.5 * c2, 0.5} : B2{1.0, c.bu, c.bv0 - c2, 1.0};
+  const bool a_if = kNeu && (k == K - 1 && hi_if);   // A_k of the right interface row
+  const bool c_if = kNeu && (k == 0 && lo_if);       // C_k of the left interface row
+  n.ap = a_if ? c.cu : c.au;
+  n.aq = a_if ? c.cv : c.av;
+  n.cp = c_if ? c.cu : c.au;
+  n.cq = c_if ? c.cv : c.av;
+  return n;
+}
+
+// One elimination step of a chain: D = B - P G, G = D^-1 Nx, z = D^-1 (r - P z).
+template <int NC>
+CHP_DEV void chain_step(bool first, B2 D, double pp, double pq, double np, double nq,
+                        double (&r)[NC][2], B2& G, double (&x)[NC][2]) {
+  if (!first) {
+    D = schur(D, pp, pq, G);
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        r[j][0] -= ap * z[j][1];
-        r[j][1] -= aq * z[j][0];
-      }
+    for (int j = 0; j < NC; ++j) {
+      r[j][0] -= pp * x[j][1];
+      r[j][1] -= pq * x[j][0];
     }
-    Di = inv2(D);
-    G = times_anti(Di, cp, cq);
-    const int ncol = kNeu ? 2 : 3;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      if (j >= ncol) break;
-      const double z0 = Di.a * r[j][0] + Di.b * r[j][1];
-      const double z1 = Di.c * r[j][0] + Di.d * r[j][1];
-      z[j][0] = z0;
-      z[j][1] = z1;
-      sc.at(k, 4 + 2 * j) = z0;
-      sc.at(k, 5 + 2 * j) = z1;
-    }
-    sc.at(k, 0) = G.a; sc.at(k, 1) = G.b; sc.at(k, 2) = G.c; sc.at(k, 3) = G.d;
   }
-  return Di;
+  const B2 Di = inv2(D);
+  G = times_anti(Di, np, nq);
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const double z0 = Di.a * r[j][0] + Di.b * r[j][1];
+    const double z1 = Di.c * r[j][0] + Di.d * r[j][1];
+    x[j][0] = z0;
+    x[j][1] = z1;
+  }
+}
+
+// Block elimination of one subdomain system (nodes k = 0..K-1 = first_node +
+// k) from BOTH ends at once, carrying NC right-hand-side columns: the forward
+// chain (from k = 0) ends with x_{K-1}, the reverse chain (from k = K-1) with
+// x_0 -- the only values the interface iteration needs, so nothing is stored;
+// the two independent chains interleave for ILP.  Row k:
+//   A_k x_{k-1} + B_k x_k + C_k x_{k+1} = r_k,   A, C = [[0, p], [q, 0]];
+// the forward chain's coupling to the previous node is A_k (next: C_k), the
+// reverse chain's C_k (next: A_k).  `kNeu`: Neumann rows (ddm.py:218-236).
+// (Interleaving the Neumann and Dirichlet systems too -- four chains -- was
+// measured slower: 198 registers, 2.33 vs 2.12 ms per config-2-shaped launch.)
+template <int NC, bool kNeu, typename Rhs>
+CHP_DEV void solve_ends(const NNConst& c, const double* u, int first_node, int K, bool lo_if,
+                        bool hi_if, Rhs rhs, double (&xf)[NC][2], double (&xr)[NC][2]) {
+  B2 Gf = {0, 0, 0, 0}, Gr = {0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < NC; ++j) xf[j][0] = xf[j][1] = xr[j][0] = xr[j][1] = 0.0;
+#pragma unroll 2
+  for (int s = 0; s < K; ++s) {
+    const int kf = s, kr = K - 1 - s;
+    const double uf = u[first_node + kf - 1], ur = u[first_node + kr - 1];
+    const NodeRow<kNeu> nf = node_row<kNeu>(c, uf * uf, kf, K, lo_if, hi_if);
+    const NodeRow<kNeu> nr = node_row<kNeu>(c, ur * ur, kr, K, lo_if, hi_if);
+    double rf[NC][2], rr[NC][2];
+    rhs(kf, uf, rf);
+    rhs(kr, ur, rr);
+    chain_step<NC>(s == 0, nf.D, nf.ap, nf.aq, nf.cp, nf.cq, rf, Gf, xf);
+    chain_step<NC>(s == 0, nr.D, nr.cp, nr.cq, nr.ap, nr.aq, rr, Gr, xr);
+  }
 }
 
 __global__ void __launch_bounds__(128) k_nn_propagate(
@@ -163,66 +190,46 @@ __global__ void __launch_bounds__(128) k_nn_propagate(
     double* o = out + (size_t)idx * out_stride;
     if (st > 0 && !c.warm) g = h = 0.0;
 
-    // ---- Neumann interface responses (ddm.py:205-256) ----
+    // ---- Neumann interface responses (ddm.py:205-256) and Dirichlet edge
+    // values + trace responses (ddm.py:147-203): only the end values of each
+    // solve are needed, so each system is eliminated once from either end ----
     double ner[4][4] = {};   // rows (phi_L, phi_R, psi_L, psi_R), cols (L_u, L_v, R_u, R_v)
     double edge0[4] = {}, er[4][4] = {};  // rows (u_first, u_last, v_first, v_last)
     double unode = 0.0, c2node = 0.0;
-    double zr[2][2] = {};    // Dirichlet right-end columns at K-1 (g_right, h_right)
     if (lane_on && live) {
       const int an = lo_if ? a : a + 1, bn = hi_if ? b : b - 1;
       const int Kn = bn - an + 1;
-      const B2 Di = eliminate<true>(c, sc, u, an, Kn, lo_if, hi_if);
-      // columns 2,3 (right loads) are zero except at K-1: z_{K-1} = Di * e
-      double x[4][2];
-      x[0][0] = sc.at(Kn - 1, 4); x[0][1] = sc.at(Kn - 1, 5);
-      x[1][0] = sc.at(Kn - 1, 6); x[1][1] = sc.at(Kn - 1, 7);
-      x[2][0] = hi_if ? Di.a : 0.0; x[2][1] = hi_if ? Di.c : 0.0;
-      x[3][0] = hi_if ? Di.b : 0.0; x[3][1] = hi_if ? Di.d : 0.0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) { ner[1][j] = x[j][0]; ner[3][j] = x[j][1]; }
-      for (int k = Kn - 2; k >= 0; --k) {
-        const double Ga = sc.at(k, 0), Gb = sc.at(k, 1), Gc = sc.at(k, 2), Gd = sc.at(k, 3);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double z0 = j < 2 ? sc.at(k, 4 + 2 * j) : 0.0;
-          const double z1 = j < 2 ? sc.at(k, 5 + 2 * j) : 0.0;
-          const double x0 = z0 - (Ga * x[j][0] + Gb * x[j][1]);
-          const double x1 = z1 - (Gc * x[j][0] + Gd * x[j][1]);
-          x[j][0] = x0;
-          x[j][1] = x1;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) { ner[0][j] = x[j][0]; ner[2][j] = x[j][1]; }
-
-      // ---- Dirichlet solution and trace responses (ddm.py:147-203) ----
+      auto neu_rhs = [&](int k, double, double (&r)[4][2]) {
+        const bool L0 = k == 0 && lo_if, R1 = k == Kn - 1 && hi_if;
+        r[0][0] = L0 ? 1.0 : 0.0; r[0][1] = 0.0;
+        r[1][0] = 0.0;            r[1][1] = L0 ? 1.0 : 0.0;
+        r[2][0] = R1 ? 1.0 : 0.0; r[2][1] = 0.0;
+        r[3][0] = 0.0;            r[3][1] = R1 ? 1.0 : 0.0;
+      };
       const int K = step - 1;
-      const B2 Dd = eliminate<false>(c, sc, u, a + 1, K, false, false);
-      zr[0][0] = Dd.b * c.rg; zr[0][1] = Dd.d * c.rg;   // g_right: v-row load
-      zr[1][0] = Dd.a * c.rh; zr[1][1] = Dd.c * c.rh;   // h_right: u-row load
-      double y[5][2];
+      auto dir_rhs = [&](int k, double un, double (&r)[5][2]) {
+        const bool f = k == 0, l = k == K - 1;
+        r[0][0] = un;             r[0][1] = -un;
+        r[1][0] = 0.0;            r[1][1] = f ? c.rg : 0.0;   // g_left  (v-row)
+        r[2][0] = f ? c.rh : 0.0; r[2][1] = 0.0;              // h_left  (u-row)
+        r[3][0] = 0.0;            r[3][1] = l ? c.rg : 0.0;   // g_right (v-row)
+        r[4][0] = l ? c.rh : 0.0; r[4][1] = 0.0;              // h_right (u-row)
+      };
+      double xf[4][2], xr[4][2];
+      solve_ends<4, true>(c, u, an, Kn, lo_if, hi_if, neu_rhs, xf, xr);
 #pragma unroll
-      for (int j = 0; j < 3; ++j) { y[j][0] = sc.at(K - 1, 4 + 2 * j); y[j][1] = sc.at(K - 1, 5 + 2 * j); }
-      y[3][0] = zr[0][0]; y[3][1] = zr[0][1];
-      y[4][0] = zr[1][0]; y[4][1] = zr[1][1];
-      edge0[1] = y[0][0]; edge0[3] = y[0][1];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) { er[1][j] = y[j + 1][0]; er[3][j] = y[j + 1][1]; }
-      for (int k = K - 2; k >= 0; --k) {
-        const double Ga = sc.at(k, 0), Gb = sc.at(k, 1), Gc = sc.at(k, 2), Gd = sc.at(k, 3);
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-          const double z0 = j < 3 ? sc.at(k, 4 + 2 * j) : 0.0;
-          const double z1 = j < 3 ? sc.at(k, 5 + 2 * j) : 0.0;
-          const double x0 = z0 - (Ga * y[j][0] + Gb * y[j][1]);
-          const double x1 = z1 - (Gc * y[j][0] + Gd * y[j][1]);
-          y[j][0] = x0;
-          y[j][1] = x1;
-        }
+      for (int j = 0; j < 4; ++j) {
+        ner[0][j] = xr[j][0]; ner[1][j] = xf[j][0];
+        ner[2][j] = xr[j][1]; ner[3][j] = xf[j][1];
       }
-      edge0[0] = y[0][0]; edge0[2] = y[0][1];
+      double yf[5][2], yr[5][2];
+      solve_ends<5, false>(c, u, a + 1, K, false, false, dir_rhs, yf, yr);
+      edge0[0] = yr[0][0]; edge0[1] = yf[0][0]; edge0[2] = yr[0][1]; edge0[3] = yf[0][1];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) { er[0][j] = y[j + 1][0]; er[2][j] = y[j + 1][1]; }
+      for (int j = 0; j < 4; ++j) {
+        er[0][j] = yr[j + 1][0]; er[1][j] = yf[j + 1][0];
+        er[2][j] = yr[j + 1][1]; er[3][j] = yf[j + 1][1];
+      }
       if (hi_if) {
         unode = u[b - 1];
         c2node = unode * unode;
@@ -297,17 +304,34 @@ __global__ void __launch_bounds__(128) k_nn_propagate(
       const double rgv = hi_if ? g : 0.0, rhv = hi_if ? h : 0.0;
       const int K = step - 1;
       bool fin = true;
-      double x0 = sc.at(K - 1, 4) + (tg * sc.at(K - 1, 6) + th * sc.at(K - 1, 8) +
-                                     rgv * zr[0][0] + rhv * zr[1][0]);
-      double x1 = sc.at(K - 1, 5) + (tg * sc.at(K - 1, 7) + th * sc.at(K - 1, 9) +
-                                     rgv * zr[0][1] + rhv * zr[1][1]);
+      // Dirichlet solve at the converged traces (= dir_sol0 + dir_response @
+      // traces): forward elimination storing G_k, z_k, then back substitution
+      B2 G = {0, 0, 0, 0};
+      double z0 = 0.0, z1 = 0.0;
+      for (int k = 0; k < K; ++k) {
+        const double un = u[a + k];
+        const double c2 = un * un;
+        B2 D = B2{1.0, c.bu, c.bv0 - c2, 1.0};
+        double r0 = un + ((k == 0 ? th * c.rh : 0.0) + (k == K - 1 ? rhv * c.rh : 0.0));
+        double r1 = -un + ((k == 0 ? tg * c.rg : 0.0) + (k == K - 1 ? rgv * c.rg : 0.0));
+        if (k > 0) {
+          D = schur(D, c.au, c.av, G);
+          r0 -= c.au * z1;
+          r1 -= c.av * z0;
+        }
+        const B2 Di = inv2(D);
+        G = times_anti(Di, c.au, c.av);
+        z0 = Di.a * r0 + Di.b * r1;
+        z1 = Di.c * r0 + Di.d * r1;
+        sc.at(k, 0) = G.a; sc.at(k, 1) = G.b; sc.at(k, 2) = G.c; sc.at(k, 3) = G.d;
+        sc.at(k, 4) = z0; sc.at(k, 5) = z1;
+      }
+      double x0 = z0, x1 = z1;
       o[a + K - 1] = x0;
       fin &= isfinite(x0);
       for (int k = K - 2; k >= 0; --k) {
-        const double z0 = sc.at(k, 4) + (tg * sc.at(k, 6) + th * sc.at(k, 8));
-        const double z1 = sc.at(k, 5) + (tg * sc.at(k, 7) + th * sc.at(k, 9));
-        const double n0 = z0 - (sc.at(k, 0) * x0 + sc.at(k, 1) * x1);
-        const double n1 = z1 - (sc.at(k, 2) * x0 + sc.at(k, 3) * x1);
+        const double n0 = sc.at(k, 4) - (sc.at(k, 0) * x0 + sc.at(k, 1) * x1);
+        const double n1 = sc.at(k, 5) - (sc.at(k, 2) * x0 + sc.at(k, 3) * x1);
         x0 = n0;
         x1 = n1;
         o[a + k] = x0;
