@@ -206,3 +206,36 @@ def test_nn_parareal_config2_grid_vs_oracle(M):
     assert np.max(np.abs(np.array(incs) - np.array(ref.increments))) < ATOL
     U = np.array([f.values for f in st.iterates])
     assert np.max(np.abs(U - ref.iterates)) < ATOL
+
+
+def test_spec_acceptance_9_nn_matches_linear_a(M):
+    """SPEC.md acceptance 9 (first half): nn_time_step matches the monodomain
+    step_linear_a to 1e-8 on 20 random states (N0 = 8, theta = 1/4, nn_tol =
+    1e-10), at the paper's section-4.6 mesh h = 1/128 and fine step 1/4000."""
+    ddm, grid, _, schemes = M
+    g = grid.SpatialGrid(1, 129)
+    dt, eps = 1.0 / 4000.0, 0.0725
+    dec, p = ddm.Decomposition(g, 8), ddm.NNParams(8, 0.25, 1e-10)
+    spec = schemes.PropagatorSpec(schemes.Scheme.LINEAR_A, dt, eps)
+    rng = np.random.default_rng(2024)
+    for _ in range(20):
+        u = grid.Field(g, rng.uniform(-1.0, 1.0, 127))
+        a = schemes.step_linear_a(u, spec)
+        b = ddm.nn_time_step(u, dec, p, dt, eps)
+        assert np.max(np.abs(a.values - b.values)) < 1e-8
+
+
+def test_spec_acceptance_9_pa1_with_nn_fine(M):
+    """SPEC.md acceptance 9 (second half): PA-I with the NN fine solver at the
+    section-4.6 configuration (T = 1, N = 20, J = 200, h = 1/128, eps = 0.0725,
+    N0 = 8, theta = 1/4) converges to tol 1e-6 against its own serial fine
+    reference with an iteration count within +-1 of plain PA-I."""
+    ddm, grid, parareal, _ = M
+    g = grid.SpatialGrid(1, 129)
+    u0 = grid.Field(g, np.random.default_rng(46).uniform(-0.05, 0.05, 127))
+    part = parareal.TimePartition(1.0, 20, 200)
+    var = parareal.AlgorithmVariant.PA1
+    plain = parareal.run(u0, var, part, 0.0725)
+    nn = parareal.run(u0, var, part, 0.0725, nn=ddm.NNParams(8, 0.25, 1e-10))
+    assert plain.converged_at is not None and nn.converged_at is not None
+    assert abs(plain.converged_at - nn.converged_at) <= 1, (plain.converged_at, nn.converged_at)
