@@ -34,6 +34,7 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kRow = 6;   // assembly scratch doubles per node: G (4) + z (2)
+constexpr int kQ = 4;     // register-queue depth of the field loads
 
 struct NNConst {
   double dt, eps2, hh, hgrid, theta, tol;
@@ -139,10 +140,25 @@ CHP_DEV void solve_ends(const NNConst& c, const double* u, int first_node, int K
   B2 Gf = {0, 0, 0, 0}, Gr = {0, 0, 0, 0};
 #pragma unroll
   for (int j = 0; j < NC; ++j) xf[j][0] = xf[j][1] = xr[j][0] = xr[j][1] = 0.0;
-#pragma unroll 2
+  // field values enter a register queue kQ nodes ahead of their use, so the
+  // loads overlap the dependent elimination chain instead of stalling it
+  const double* uf0 = u + first_node - 1;        // node k -> uf0[k]
+  double qf[kQ], qr[kQ];
+#pragma unroll
+  for (int t = 0; t < kQ; ++t) {
+    qf[t] = t < K ? uf0[t] : 0.0;
+    qr[t] = t < K ? uf0[K - 1 - t] : 0.0;
+  }
   for (int s = 0; s < K; ++s) {
     const int kf = s, kr = K - 1 - s;
-    const double uf = u[first_node + kf - 1], ur = u[first_node + kr - 1];
+    const double uf = qf[0], ur = qr[0];
+#pragma unroll
+    for (int t = 0; t + 1 < kQ; ++t) {
+      qf[t] = qf[t + 1];
+      qr[t] = qr[t + 1];
+    }
+    qf[kQ - 1] = s + kQ < K ? uf0[s + kQ] : 0.0;
+    qr[kQ - 1] = s + kQ < K ? uf0[K - 1 - s - kQ] : 0.0;
     const NodeRow<kNeu> nf = node_row<kNeu>(c, uf * uf, kf, K, lo_if, hi_if);
     const NodeRow<kNeu> nr = node_row<kNeu>(c, ur * ur, kr, K, lo_if, hi_if);
     double rf[NC][2], rr[NC][2];
@@ -308,8 +324,15 @@ __global__ void __launch_bounds__(128) k_nn_propagate(
       // traces): forward elimination storing G_k, z_k, then back substitution
       B2 G = {0, 0, 0, 0};
       double z0 = 0.0, z1 = 0.0;
+      const double* ua = u + a;                 // node a+1+k -> ua[k]
+      double q[kQ];
+#pragma unroll
+      for (int t = 0; t < kQ; ++t) q[t] = t < K ? ua[t] : 0.0;
       for (int k = 0; k < K; ++k) {
-        const double un = u[a + k];
+        const double un = q[0];
+#pragma unroll
+        for (int t = 0; t + 1 < kQ; ++t) q[t] = q[t + 1];
+        q[kQ - 1] = k + kQ < K ? ua[k + kQ] : 0.0;
         const double c2 = un * un;
         B2 D = B2{1.0, c.bu, c.bv0 - c2, 1.0};
         double r0 = un + ((k == 0 ? th * c.rh : 0.0) + (k == K - 1 ? rhv * c.rh : 0.0));
@@ -329,9 +352,22 @@ __global__ void __launch_bounds__(128) k_nn_propagate(
       double x0 = z0, x1 = z1;
       o[a + K - 1] = x0;
       fin &= isfinite(x0);
+      // back substitution; node k-1's G, z are loaded while node k is solved
+      double gz[6];
+      if (K >= 2) {
+#pragma unroll
+        for (int f = 0; f < 6; ++f) gz[f] = sc.at(K - 2, f);
+      }
       for (int k = K - 2; k >= 0; --k) {
-        const double n0 = sc.at(k, 4) - (sc.at(k, 0) * x0 + sc.at(k, 1) * x1);
-        const double n1 = sc.at(k, 5) - (sc.at(k, 2) * x0 + sc.at(k, 3) * x1);
+        double cur[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) cur[f] = gz[f];
+        if (k >= 1) {
+#pragma unroll
+          for (int f = 0; f < 6; ++f) gz[f] = sc.at(k - 1, f);
+        }
+        const double n0 = cur[4] - (cur[0] * x0 + cur[1] * x1);
+        const double n1 = cur[5] - (cur[2] * x0 + cur[3] * x1);
         x0 = n0;
         x1 = n1;
         o[a + k] = x0;
