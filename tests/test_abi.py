@@ -41,6 +41,10 @@ def test_null_context_rejected():
     lib = N.load_library()
     assert lib.chp_propagate(None, None, None, 1, 1, None, 0, None, 0, None, None, None) == 1
     assert lib.chp_ctx_create(0, None) == 1
+    assert lib.chp_nn_propagate(None, None, None, 1e-4, 1e-3, 1, 1, None, 0, None, 0, None, None,
+                                None, None, None) == 1
+    assert lib.chp_newton_history(None, None, 0) == 1
+    assert ctypes.sizeof(N.ChpNNParams) == 4 * 4 + 3 * 8
 
 
 @pytest.mark.parametrize("nx", [4, 5, 10, 17, 257, 1025, 1000])
