@@ -90,18 +90,33 @@ class ShardedParareal:
         self.eng.changed.fill_(1)        # every F(U_n^0) is needed at k = 0
         self.k = 0
 
-    def iterate(self, force_all: bool = False, coarse_after=None, defer: bool = False):
+    def iterate(self, force_all: bool = False, coarse_after=None, defer: bool = False,
+                fine_chunks=None, coarse_chunks=None, on_coarse_chunk=None):
         """One Parareal iteration.  ``coarse_after``: an optional CUDA event the
         coarse sweep waits for (an input copy overlapped with the fine sweep).
         ``defer``: do not wait for the all-ranks increment (returns None; call
         ``flush()``): rank r then starts iteration k+1 as soon as its own part of
         the coarse chain of iteration k is done, while ranks r+1.. are still in
-        the chain (pipelined Parareal across ranks; same arithmetic)."""
+        the chain (pipelined Parareal across ranks; same arithmetic).
+        ``fine_chunks``: [(lo, hi, event)] -- the fine sweep runs slice range
+        [lo, hi) after ``event`` (its inputs' copy) completes; ``coarse_chunks``:
+        [(n0, n1)] -- the coarse sweep runs in these consecutive ranges, calling
+        ``on_coarse_chunk(n0, n1)`` after each (e.g. to start copying the
+        finished iterates out).  Same arithmetic as one sweep."""
         eng = self.eng
         flags = eng.changed.cpu().numpy()
         if force_all:
             flags[:, : self.local_slices] |= 1
-        eng.fine_sweep(flags)
+        if fine_chunks is None:
+            eng.fine_sweep(flags)
+        else:
+            for lo, hi, ev in fine_chunks:
+                if ev is not None:
+                    self._torch.cuda.current_stream().wait_event(ev)
+                part = np.zeros_like(flags)
+                part[:, lo:hi] = flags[:, lo:hi]
+                part[:, 0] |= flags[:, 0] & 2
+                eng.fine_sweep(part)
         if coarse_after is not None:
             self._torch.cuda.current_stream().wait_event(coarse_after)
         eng.inc.zero_()
@@ -110,7 +125,13 @@ class ShardedParareal:
             eng.changed[0, 0] = 1 if force_all else 0
         elif force_all:
             eng.changed[0, 0] = 1
-        eng.coarse_range(1, 0, self.local_slices)
+        if coarse_chunks is None:
+            eng.coarse_range(1, 0, self.local_slices)
+        else:
+            for n0, n1 in coarse_chunks:
+                eng.coarse_range(1, n0, n1)
+                if on_coarse_chunk is not None:
+                    on_coarse_chunk(n0, n1)
         self._send_boundary()
         eng.check_status()
         inc = eng.inc.clone()
@@ -168,13 +189,17 @@ class ShardedParareal:
         torch.cuda.synchronize()
         return a.elapsed_time(b)
 
-    def e2e_step_rate(self, steps: int, warmup: int = 1) -> dict:
+    def e2e_step_rate(self, steps: int, warmup: int = 1, chunks: int = 2,
+                      coarse_chunked: bool = True) -> dict:
         """Same metric with host-resident iterates: per step the local iterates
         and coarse values are copied H2D from pinned memory, one forced
         iteration runs, and the new iterates are copied back D2H.  The coarse
         values are only read by the coarse sweep, so their copy runs on a side
-        stream under the fine sweep; the iterates' copies are on the critical
-        path (the fine sweep reads U, the result is U^{k+1})."""
+        stream under the fine sweep.  The iterates move in ``chunks`` slice
+        ranges: chunk c+1 is copied in while the fine sweep of chunk c runs, and
+        the coarse sweep runs chunk by chunk with each finished range copied out
+        under the next range's sweep -- only the first chunk's input and the
+        last chunk's output copies stay exposed."""
         torch = self._torch
         eng = self.eng
         hU = torch.empty(eng.U.shape, dtype=torch.float64, pin_memory=True)
@@ -183,29 +208,66 @@ class ShardedParareal:
         hU.copy_(eng.U)
         hG.copy_(eng.G)
         side = torch.cuda.Stream(device=eng.U.device)
+        h2d = torch.cuda.Stream(device=eng.U.device)
+        d2h = torch.cuda.Stream(device=eng.U.device)
         main = torch.cuda.current_stream()
+        L = self.local_slices
+        nch = max(1, min(chunks, L))
+        bounds = [L * c // nch for c in range(nch + 1)]
 
         def step():
-            eng.U.copy_(hU, non_blocking=True)
+            # U^k in slice chunks on a copy stream; the fine sweep of chunk c
+            # starts when its rows have landed (chunk c+1 copies meanwhile)
+            h2d.wait_stream(main)
+            h2d.wait_stream(d2h)                      # last step's read-out of U is done
+            fine = []
+            with torch.cuda.stream(h2d):
+                for c in range(nch):
+                    lo, hi = bounds[c], bounds[c + 1]
+                    r1 = hi + 1 if c == nch - 1 else hi   # last chunk: U[L] as well
+                    eng.U[:, lo:r1].copy_(hU[:, lo:r1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(h2d)
+                    fine.append((lo, hi, ev))
             side.wait_stream(main)                    # G is free: the last sweep is done
             with torch.cuda.stream(side):
                 eng.G.copy_(hG, non_blocking=True)
                 g_ready = torch.cuda.Event()
                 g_ready.record(side)
-            self.iterate(force_all=True, coarse_after=g_ready, defer=True)
+            # (the last fine chunk waits for the last copy event, so the whole of
+            # U is resident before the coarse sweep)
+
+            def out_chunk(n0, n1):
+                # U^{k+1}_{n0+1..n1} are final: copy them out under the next chunk's
+                # coarse sweep (U_0 with the first chunk)
+                ev = torch.cuda.Event()
+                ev.record(main)
+                d2h.wait_event(ev)
+                r0 = 0 if n0 == 0 else n0 + 1
+                with torch.cuda.stream(d2h):
+                    hOut[:, r0:n1 + 1].copy_(eng.U[:, r0:n1 + 1], non_blocking=True)
+
             # the result U^{k+1} goes to its own buffer: every step starts from the
             # same consistent host state (U^k, G(U^k))
-            hOut.copy_(eng.U, non_blocking=True)
+            if coarse_chunked:
+                self.iterate(force_all=True, coarse_after=g_ready, defer=True, fine_chunks=fine,
+                             coarse_chunks=[(bounds[c], bounds[c + 1]) for c in range(nch)],
+                             on_coarse_chunk=out_chunk)
+            else:
+                self.iterate(force_all=True, coarse_after=g_ready, defer=True, fine_chunks=fine)
+                out_chunk(0, L)
 
         for _ in range(warmup):
             step()
         self.flush()
         torch.cuda.synchronize()
+        assert torch.equal(hOut.to(eng.U.device), eng.U), "e2e read-out differs from U"
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(steps):
             step()
         self.flush()
+        main.wait_stream(d2h)
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / steps

@@ -121,21 +121,30 @@ def _worker_defer(rank, world, port, out_q):
     f, c = P.propagator_pair(P.AlgorithmVariant("pa3"), part, 0.1)
     u0 = np.random.default_rng(3).uniform(-0.5, 0.5, 15)
     res = []
-    for defer in (False, True):
+    for mode in ("sync", "defer", "chunked"):
         sh = ShardedParareal(g, f, c, 4, 4, rank=rank, world=world, engine_factory=HostEngine)
         sh.load(Field(g, u0))
         sh.coarse_init()
+        seen = []
         for _ in range(3):
-            sh.iterate(force_all=True, defer=defer)
+            if mode == "chunked":     # the e2e step's slice-chunked fine and coarse sweeps
+                sh.iterate(force_all=True, defer=True, fine_chunks=[(0, 1, None), (1, 2, None)],
+                           coarse_chunks=[(0, 1), (1, 2)],
+                           on_coarse_chunk=lambda n0, n1: seen.append((n0, n1)))
+            else:
+                sh.iterate(force_all=True, defer=(mode == "defer"))
         sh.flush()
+        if mode == "chunked":
+            assert seen == [(0, 1), (1, 2)] * 3
         res.append((sh.k, list(sh.increments), sh.local_iterates()))
     out_q.put((rank, res))
     dist.destroy_process_group()
 
 
 def test_two_rank_deferred_increments_match():
-    """iterate(defer=True) (the bench's pipelined step) computes exactly what the
-    synchronous iteration computes: same iterates bit for bit, same increments."""
+    """iterate(defer=True) (the bench's pipelined step) and the e2e step's
+    slice-chunked sweeps compute exactly what the synchronous iteration computes:
+    same iterates bit for bit, same increments."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 30500 + (os.getpid() % 1000)
@@ -146,7 +155,8 @@ def test_two_rank_deferred_increments_match():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, (sync, deferred) in out:
-        assert sync[0] == deferred[0] == 3
-        assert sync[1] == deferred[1]
-        assert np.array_equal(sync[2], deferred[2])
+    for rank, (sync, deferred, chunked) in out:
+        for other in (deferred, chunked):
+            assert sync[0] == other[0] == 3
+            assert sync[1] == other[1]
+            assert np.array_equal(sync[2], other[2])
