@@ -280,4 +280,5 @@ class ShardedParareal:
         return {"value": pts / (ms * 1e-3), "unit": "grid-point-steps/s",
                 "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": nbytes,
                 "ms_per_step": ms,
-                "path": "pinned host iterates -> engine (chp_propagate/chp_coarse_sweep) -> host"}
+                "path": "pinned host iterates -> engine (chp_propagate/chp_coarse_sweep) -> host",
+                "copies": f"{nch} slice chunks, overlapped with the fine and coarse sweeps"}
