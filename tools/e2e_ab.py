@@ -19,7 +19,7 @@ fine, coarse = P.propagator_pair(P.AlgorithmVariant.PA3, part, cfg["eps"])
 eng = ShardedParareal(g, fine, coarse, cfg["N"], cfg["J"])
 eng.load(Field(g, O.initial_condition(5)))
 eng.coarse_init()
-for ch, cc in [(1, False), (8, False), (2, True), (8, True), (1, False)]:
+for ch, cc in [(2, True), (3, True), (4, True), (2, True), (4, True)]:
     r = eng.e2e_step_rate(2, chunks=ch, coarse_chunked=cc)
     print(json.dumps({"chunks": ch, "coarse_chunked": cc, "ms": r["ms_per_step"],
                       "value": r["value"]}), flush=True)
