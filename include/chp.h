@@ -100,8 +100,12 @@ const char* chp_version(void);
 const char* chp_status_str(int status);
 
 /* Create a context on `device`: owns cached solver tables (the analogue of
- * schemes._FACTOR_CACHE, schemes.py:134-142) and scratch.  Not thread safe;
- * one per device/process. */
+ * schemes._FACTOR_CACHE, schemes.py:134-142) and scratch.  One per device per
+ * process.  Every entry point locks the context (calls from several host
+ * threads serialise; the reference calls propagate from worker threads,
+ * SPEC.md:163) and runs on the context's device whatever device is current,
+ * restoring the caller's current device on return; `stream` must belong to that
+ * device. */
 chp_status chp_ctx_create(int device, chp_ctx** out);
 chp_status chp_ctx_destroy(chp_ctx* ctx);
 const char* chp_last_error(chp_ctx* ctx);
@@ -156,14 +160,20 @@ chp_status chp_max_abs_diff(chp_ctx* ctx, const chp_grid* g, int n_fields,
                             double* out, void* stream);
 
 /*
- * chp_newton_history -- register (hist != NULL) or clear (NULL) a caller-owned
- * device buffer that receives StepReport.residual_history (schemes.py:285-290):
- * for every system idx(s) advanced by a later NONLINEAR_EYRE chp_propagate on
- * this context, hist[idx * hist_len + it] = the residual norm before Newton
- * solve `it` (it < hist_len) of its last step; entries after the accepted (or
- * failing) iteration are left untouched.  Not used by chp_coarse_sweep.
+ * chp_propagate_hist -- chp_propagate that also records StepReport.residual_history
+ * (schemes.py:285-290) of a NONLINEAR_EYRE propagation: for every system idx(s),
+ * hist[idx * hist_len + it] = the residual norm before Newton solve `it`
+ * (it < hist_len) of its last step; entries after the accepted (or failing)
+ * iteration are left untouched.  `hist` (caller-owned device buffer, or NULL) is
+ * used by this call only; other schemes ignore it.  Replaces the per-step
+ * report of step_nonlinear (schemes.py:270-305).
  */
-chp_status chp_newton_history(chp_ctx* ctx, double* hist, int hist_len);
+chp_status chp_propagate_hist(chp_ctx* ctx, const chp_grid* g, const chp_spec* spec,
+                              int steps, int nsys,
+                              const double* in, long long in_stride,
+                              double* out, long long out_stride,
+                              const int* sys_index, chp_sys_info* info,
+                              double* hist, int hist_len, void* stream);
 
 /* Neumann-Neumann interface-iteration parameters (ddm.py:51-66, NNParams)
  * plus h**2 formed by the caller as grid.h**2 (ddm.py:274). */

@@ -24,7 +24,7 @@ SYS_OK, SYS_NEWTON, SYS_NONFINITE, SYS_SINGULAR, SYS_CG, SYS_NN = 0, 1, 2, 3, 4,
 EXPORTS = (
     "chp_version", "chp_status_str", "chp_ctx_create", "chp_ctx_destroy", "chp_last_error",
     "chp_sysinfo_reset", "chp_propagate", "chp_coarse_sweep", "chp_max_abs_diff",
-    "chp_debug_trace", "chp_nn_propagate", "chp_newton_history",
+    "chp_debug_trace", "chp_nn_propagate", "chp_propagate_hist",
 )
 
 
@@ -87,7 +87,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                    vp, vp, vp, ll, ll, vp, vp, vp, vp]
     L.chp_max_abs_diff.argtypes = [vp, C.POINTER(ChpGrid), i, vp, ll, vp, ll, vp, vp]
     L.chp_debug_trace.argtypes = [vp, i]
-    L.chp_newton_history.argtypes = [vp, vp, i]
+    L.chp_propagate_hist.argtypes = [vp, C.POINTER(ChpGrid), C.POINTER(ChpSpec), i, i, vp, ll,
+                                     vp, ll, vp, vp, vp, i, vp]
     L.chp_nn_propagate.argtypes = [vp, C.POINTER(ChpGrid), C.POINTER(ChpNNParams), d, d, i, i,
                                    vp, ll, vp, ll, vp, vp, vp, vp, vp]
     for name in EXPORTS:
@@ -151,9 +152,12 @@ class Context:
             self.h = None
 
 
-def stream_ptr(stream=None) -> C.c_void_p:
+def stream_ptr(stream=None, device=None) -> C.c_void_p:
+    """The given stream, or the current stream of ``device`` (a torch device, an
+    index or None for the current device): the native entry points run on the
+    context's device, so the default stream must be that device's."""
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return C.c_void_p(s.cuda_stream)
 
 

@@ -399,7 +399,7 @@ struct Scratch1 {   // per-launch interleaved scratch
   double* yh;       // [m][nthreads]
   double* tmp;      // [m][nthreads] (coarse sweep: g)
   long long ks;     // nthreads
-  double* hist;     // Newton residual history [nsys'][hlen] (chp_newton_history) or null
+  double* hist;     // Newton residual history [nsys'][hlen] (chp_propagate_hist) or null
   int hlen;
 };
 

@@ -28,6 +28,15 @@ namespace {
 
 constexpr int kMinN = 8;
 constexpr int kMaxN = 1024;
+constexpr int kMaxDev = 64;
+
+// per-device one-time launch setup (function attributes, occupancy) is indexed by
+// the current device: the C ABI switches to the context's device on entry
+int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDev) ? d : 0;
+}
 
 // LINEAR_B divisors in the column pass's post-processing order (chp_linb.cuh):
 // for column pair qp, lane l of L, r = 2j + h < 2C: (D''(p, 2qp), D''(p, 2qp+1)),
@@ -493,8 +502,8 @@ struct Chp2d {
   struct DTab { int N; double a2dt, b; double* d; };
   std::vector<DTab> dtabs;        // LINEAR_B spectral divisors, one per (N, dt, eps)
   void* coarse = nullptr;         // v2 coarse-sweep workspace
-  double* hist = nullptr;         // Newton residual history (chp_newton_history), caller owned
-  int hlen = 0;
+  double* hist = nullptr;         // Newton residual history of the current chp_propagate_hist
+  int hlen = 0;                   // call (caller owned; null outside that call)
   size_t coarse_bytes = 0;
   void* pcg = nullptr;            // v2 batched PCG workspace
   size_t pcg_bytes = 0;
@@ -504,11 +513,6 @@ struct Chp2d {
 };
 
 Chp2d* chp2d_create() { return new Chp2d(); }
-
-void chp2d_set_history(Chp2d* c, double* hist, int hlen) {
-  c->hist = hist;
-  c->hlen = hlen;
-}
 
 void chp2d_destroy(Chp2d* c) {
   if (!c) return;
@@ -627,7 +631,8 @@ template <int N>
 cudaError_t pcg_solve2(Chp2d* cx, const chp_grid& g, int nsys, double a, double b, double tol,
                        int max_iter, const NTables& nt, Work2& W, cudaStream_t st, int warm) {
   using G2 = Pcg2G<N>;
-  static bool attrs = false;
+  static bool attrs_dev[kMaxDev] = {};
+  bool& attrs = attrs_dev[cur_dev()];
   if (!attrs) {
     const int sm = (int)G2::SMEM;
     cudaFuncSetAttribute(k_pcg2_rows<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -856,7 +861,8 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
                           double* scratch, const double* dtab, cudaStream_t st) {
   using RG = linb::RowG<N>;
   using CG = linb::ColG<N>;
-  static bool attrs = false;
+  static bool attrs_dev[kMaxDev] = {};
+  bool& attrs = attrs_dev[cur_dev()];
   if (!attrs) {
     cudaFuncSetAttribute(linb::k2d_rowb<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
     cudaFuncSetAttribute(linb::k2d_colb<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
@@ -914,7 +920,8 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
   // propagate per slice + the correction kernel below
   if (sp.scheme == CHP_LINEAR_A) {
     using G2 = Coop2G<N>;
-    static int blocks = 0;
+    static int blocks_dev[kMaxDev] = {};
+    int& blocks = blocks_dev[cur_dev()];
     if (blocks == 0) {
       cudaFuncSetAttribute(k2d_coarse2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)G2::SMEM);
@@ -1015,12 +1022,19 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
 cudaError_t chp2d_propagate(Chp2d* c, const chp_grid& g, const chp_spec& sp, int steps, int nsys,
                             const double* in, long long in_stride, double* out,
                             long long out_stride, const int* sys_index, chp_sys_info* info,
-                            cudaStream_t st, std::string* err) {
+                            double* hist, int hlen, cudaStream_t st, std::string* err) {
   if (!pow2_ok(g, err)) return cudaSuccess;
   const int N = g.m + 1;
   const NTables* nt = nullptr;
   cudaError_t e = get_tables(c, N, &nt);
   if (e != cudaSuccess) return e;
+  // the history buffer belongs to this call only (the caller holds the context lock)
+  struct HistScope {
+    Chp2d* c;
+    ~HistScope() { c->hist = nullptr; c->hlen = 0; }
+  } hs{c};
+  c->hist = hist;
+  c->hlen = hist ? hlen : 0;
   CHP_N_SWITCH(N, return propagate_n<NN>(c, g, sp, steps, nsys, in, in_stride, out, out_stride,
                                          sys_index, info, *nt, st));
   *err = "unsupported N";
@@ -1037,6 +1051,8 @@ cudaError_t chp2d_coarse_sweep(Chp2d* c, const chp_grid& g, const chp_spec& sp, 
   const NTables* nt = nullptr;
   cudaError_t e = get_tables(c, N, &nt);
   if (e != cudaSuccess) return e;
+  c->hist = nullptr;            // coarse steps never record a residual history
+  c->hlen = 0;
   CHP_N_SWITCH(N, return sweep_n<NN>(c, g, sp, mode, nic, nsl, n0, n1, U, F, G, ic_stride,
                                      sl_stride, changed, inc, info, *nt, st));
   *err = "unsupported N";

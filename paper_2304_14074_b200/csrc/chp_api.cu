@@ -3,6 +3,7 @@
 #include <string.h>
 
 #include <map>
+#include <mutex>
 #include <string>
 #include <tuple>
 
@@ -33,11 +34,10 @@ cudaError_t chp_nn_launch(const chp_grid& gr, const chp_nn_params& p, double dt,
 struct Chp2d;
 Chp2d* chp2d_create();
 void chp2d_destroy(Chp2d*);
-void chp2d_set_history(Chp2d*, double* hist, int hlen);
 cudaError_t chp2d_propagate(Chp2d* c, const chp_grid& g, const chp_spec& sp, int steps, int nsys,
                             const double* in, long long in_stride, double* out,
                             long long out_stride, const int* sys_index, chp_sys_info* info,
-                            cudaStream_t st, std::string* err);
+                            double* hist, int hlen, cudaStream_t st, std::string* err);
 cudaError_t chp2d_coarse_sweep(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode,
                                int nic, int nsl, int n0, int n1, double* U, const double* F,
                                double* G, long long ic_stride, long long sl_stride,
@@ -54,8 +54,25 @@ struct chp_ctx {
   size_t scratch_bytes = 0;
   int* dev_err = nullptr;
   Chp2d* d2 = nullptr;
-  double* hist = nullptr;   // chp_newton_history buffer (caller owned)
-  int hlen = 0;
+  // every entry point holds the lock from argument checks through the launches:
+  // the factor map, scratch, 2D workspaces and last_error are shared state (the
+  // reference calls propagate from worker threads)
+  std::mutex mu;
+};
+
+// Switch to the context's device for the duration of an entry point and restore
+// the caller's current device afterwards (kernels, caches and scratch all live on
+// ctx->device whatever device the caller has current).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
 };
 
 namespace {
@@ -151,8 +168,11 @@ const char* chp_status_str(int s) {
 chp_status chp_ctx_create(int device, chp_ctx** out) {
   if (!out) return CHP_ERR_ARG;
   *out = nullptr;
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) return CHP_ERR_CUDA;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return CHP_ERR_CUDA;
+  DeviceGuard dg(device);
+  cudaError_t e = cudaSuccess;
   chp_ctx* c = new chp_ctx();
   c->device = device;
   e = cudaMalloc(&c->dev_err, sizeof(int) * 4);
@@ -164,7 +184,7 @@ chp_status chp_ctx_create(int device, chp_ctx** out) {
 
 chp_status chp_ctx_destroy(chp_ctx* c) {
   if (!c) return CHP_OK;
-  cudaSetDevice(c->device);
+  DeviceGuard dg(c->device);
   cudaDeviceSynchronize();
   for (auto& kv : c->factors) cudaFree(kv.second);
   if (c->scratch) cudaFree(c->scratch);
@@ -174,24 +194,37 @@ chp_status chp_ctx_destroy(chp_ctx* c) {
   return CHP_OK;
 }
 
-const char* chp_last_error(chp_ctx* c) { return c ? c->last_error.c_str() : "null context"; }
+// The returned pointer stays valid until the next failing call on the context.
+const char* chp_last_error(chp_ctx* c) {
+  if (!c) return "null context";
+  std::lock_guard<std::mutex> lk(c->mu);
+  return c->last_error.c_str();
+}
 
 chp_status chp_sysinfo_reset(chp_ctx* c, chp_sys_info* info, int n, void* stream) {
+  if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
   if (!info || n < 0) return fail(c, CHP_ERR_ARG, "bad sysinfo array");
   cudaError_t e = cudaMemsetAsync(info, 0, sizeof(chp_sys_info) * (size_t)n,
                                   (cudaStream_t)stream);
   return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "sysinfo reset");
 }
 
-chp_status chp_propagate(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int steps, int nsys,
-                         const double* in, long long in_stride, double* out,
-                         long long out_stride, const int* sys_index, chp_sys_info* info,
-                         void* stream) {
+chp_status chp_propagate_hist(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int steps,
+                              int nsys, const double* in, long long in_stride, double* out,
+                              long long out_stride, const int* sys_index, chp_sys_info* info,
+                              double* hist, int hist_len, void* stream) {
   if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
   std::string why;
   if (!grid_ok(g, &why) || !spec_ok(sp, &why)) return fail(c, CHP_ERR_ARG, why);
   if (steps < 1) return fail(c, CHP_ERR_ARG, "steps must be at least 1");
   if (nsys < 0 || !in || !out || !info) return fail(c, CHP_ERR_ARG, "bad arrays");
+  if (hist && hist_len < 1) return fail(c, CHP_ERR_ARG, "hist_len must be at least 1");
+  if (!hist) hist_len = 0;
+  if (sp->scheme != CHP_NONLINEAR_EYRE) { hist = nullptr; hist_len = 0; }
   if (nsys == 0) return CHP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (g->dim == 1) {
@@ -207,13 +240,21 @@ chp_status chp_propagate(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int 
     double* yh = ub + (size_t)g->m * 7 * nsys;
     double* tmp = yh + (size_t)g->m * nsys;
     cudaError_t e = chp1d_propagate(*g, *sp, steps, nsys, in, in_stride, out, out_stride,
-                                    sys_index, fac, ub, yh, tmp, info, st, c->hist, c->hlen);
+                                    sys_index, fac, ub, yh, tmp, info, st, hist, hist_len);
     return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp1d_propagate");
   }
   cudaError_t e = chp2d_propagate(c->d2, *g, *sp, steps, nsys, in, in_stride, out, out_stride,
-                                  sys_index, info, st, &why);
+                                  sys_index, info, hist, hist_len, st, &why);
   if (!why.empty()) return fail(c, CHP_ERR_UNSUPPORTED, why);
   return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp2d_propagate");
+}
+
+chp_status chp_propagate(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int steps, int nsys,
+                         const double* in, long long in_stride, double* out,
+                         long long out_stride, const int* sys_index, chp_sys_info* info,
+                         void* stream) {
+  return chp_propagate_hist(c, g, sp, steps, nsys, in, in_stride, out, out_stride, sys_index,
+                            info, nullptr, 0, stream);
 }
 
 chp_status chp_coarse_sweep(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int mode, int nic,
@@ -221,6 +262,8 @@ chp_status chp_coarse_sweep(chp_ctx* c, const chp_grid* g, const chp_spec* sp, i
                             long long ic_stride, long long sl_stride, unsigned char* changed,
                             double* inc, chp_sys_info* info, void* stream) {
   if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
   std::string why;
   if (!grid_ok(g, &why) || !spec_ok(sp, &why)) return fail(c, CHP_ERR_ARG, why);
   if (mode != 0 && mode != 1) return fail(c, CHP_ERR_ARG, "mode must be 0 or 1");
@@ -256,6 +299,8 @@ chp_status chp_max_abs_diff(chp_ctx* c, const chp_grid* g, int n_fields, const d
                             long long as, const double* b, long long bs, double* out,
                             void* stream) {
   if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
   std::string why;
   if (!grid_ok(g, &why)) return fail(c, CHP_ERR_ARG, why);
   if (n_fields < 0 || !a || !b || !out) return fail(c, CHP_ERR_ARG, "bad arrays");
@@ -270,6 +315,8 @@ chp_status chp_nn_propagate(chp_ctx* c, const chp_grid* g, const chp_nn_params* 
                             const int* sys_index, const double* traces_in, double* traces_out,
                             chp_sys_info* info, void* stream) {
   if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
   std::string why;
   if (!grid_ok(g, &why)) return fail(c, CHP_ERR_ARG, why);
   if (!nn) return fail(c, CHP_ERR_ARG, "null nn params");
@@ -302,15 +349,6 @@ chp_status chp_nn_propagate(chp_ctx* c, const chp_grid* g, const chp_nn_params* 
   cudaError_t e = chp_nn_launch(*g, *nn, dt, eps2, steps, nsys, in, in_stride, out, out_stride,
                                 sys_index, traces_in, traces_out, info, c->scratch, st);
   return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp_nn_propagate");
-}
-
-chp_status chp_newton_history(chp_ctx* c, double* hist, int hist_len) {
-  if (!c) return CHP_ERR_ARG;
-  if (hist && hist_len < 1) return fail(c, CHP_ERR_ARG, "hist_len must be at least 1");
-  c->hist = hist;
-  c->hlen = hist ? hist_len : 0;
-  chp2d_set_history(c->d2, c->hist, c->hlen);
-  return CHP_OK;
 }
 
 }  // extern "C"

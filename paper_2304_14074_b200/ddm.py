@@ -138,7 +138,7 @@ def nn_propagate_batch(grid: SpatialGrid, params: NNParams, dt: float, eps: floa
     st = ctx.L.chp_nn_propagate(ctx.h, native_grid(grid), _native_params(grid, params),
                                 float(dt), float(eps ** 2), int(steps), nsys, N.ptr(src), fs,
                                 N.ptr(out), fs, N.ptr(sys_index), N.ptr(traces_in),
-                                N.ptr(traces_out), N.ptr(info), N.stream_ptr(stream))
+                                N.ptr(traces_out), N.ptr(info), N.stream_ptr(stream, src.device))
     ctx.check(st, "chp_nn_propagate")
     return info
 

@@ -119,7 +119,7 @@ class PararealEngine:
         st = self.ctx.L.chp_coarse_sweep(
             self.ctx.h, self._native_grid(), self.coarse.native(), mode, self.B, self.N, n0, n1,
             N.ptr(self.U), N.ptr(self.F), N.ptr(self.G), (self.N + 1) * self.fs, self.fs,
-            N.ptr(self.changed), N.ptr(self.inc), N.ptr(self.info_coarse), N.stream_ptr())
+            N.ptr(self.changed), N.ptr(self.inc), N.ptr(self.info_coarse), N.stream_ptr(None, self.device))
         self.ctx.check(st, "chp_coarse_sweep")
 
     def _raise(self, info_t, spec, labels=None):

@@ -269,6 +269,7 @@ class RunTrace:
     newton: NewtonStats
     increments: tuple = ()
     fine_point_steps: int = 0
+    engine: object = field(default=None, repr=False)   # device state of the final iterate
 
     @property
     def errors(self) -> tuple:
@@ -339,7 +340,7 @@ def run(u0: Field, variant: AlgorithmVariant, partition: TimePartition, eps: flo
     return RunTrace(records=records, converged_at=converged_at, tolerance=tol,
                     reference_seconds=reference_seconds, reference_norm=reference_norm,
                     newton=stats, increments=tuple(float(x[0]) for x in eng.increments),
-                    fine_point_steps=eng.stats.fine_point_steps)
+                    fine_point_steps=eng.stats.fine_point_steps, engine=eng)
 
 
 @dataclass

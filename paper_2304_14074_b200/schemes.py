@@ -190,13 +190,15 @@ def raise_on_status(info: np.ndarray, spec: PropagatorSpec, labels=None) -> None
 
 
 def propagate_batch(grid: SpatialGrid, spec: PropagatorSpec, steps: int, src, out,
-                    sys_index=None, info=None, stream=None, ctx=None):
+                    sys_index=None, info=None, stream=None, ctx=None, hist=None):
     """Advance ``steps`` steps on a batch of device fields (async).
 
     ``src``/``out``: CUDA float64 tensors whose leading dimension enumerates
     fields of ``grid.device_size`` doubles (contiguous).  ``sys_index``: int32
     CUDA tensor selecting which fields to advance (default all).  ``info``:
-    ``new_sysinfo(len(src))`` tensor accumulating per-field outcomes.
+    ``new_sysinfo(len(src))`` tensor accumulating per-field outcomes.  ``hist``:
+    optional float64 CUDA tensor of nsys x hist_len receiving the Newton residual
+    history of the last step (chp_propagate_hist).
     """
     if steps < 1:
         raise ValueError(f"steps must be at least 1, got {steps}")
@@ -210,9 +212,15 @@ def propagate_batch(grid: SpatialGrid, spec: PropagatorSpec, steps: int, src, ou
     nsys = nfields if sys_index is None else int(sys_index.numel())
     if info is None:
         info = new_sysinfo(nfields, src.device)
-    st = ctx.L.chp_propagate(ctx.h, native_grid(grid), spec.native(), int(steps), nsys,
-                             N.ptr(src), fs, N.ptr(out), fs, N.ptr(sys_index), N.ptr(info),
-                             N.stream_ptr(stream))
+    if hist is None:
+        st = ctx.L.chp_propagate(ctx.h, native_grid(grid), spec.native(), int(steps), nsys,
+                                 N.ptr(src), fs, N.ptr(out), fs, N.ptr(sys_index), N.ptr(info),
+                                 N.stream_ptr(stream, src.device))
+    else:
+        st = ctx.L.chp_propagate_hist(ctx.h, native_grid(grid), spec.native(), int(steps), nsys,
+                                      N.ptr(src), fs, N.ptr(out), fs, N.ptr(sys_index),
+                                      N.ptr(info), N.ptr(hist), int(hist.numel() // max(nsys, 1)),
+                                      N.stream_ptr(stream, src.device))
     _check_ctx(ctx, st, "chp_propagate")
     return info
 
@@ -229,11 +237,11 @@ def _check_ctx(ctx, st, what):
 # reference-shaped single-field entry points
 # ---------------------------------------------------------------------------
 
-def _run_one(u: Field, spec: PropagatorSpec, steps: int):
+def _run_one(u: Field, spec: PropagatorSpec, steps: int, hist=None):
     import torch
     src = u.device_values()
     out = torch.empty_like(src)
-    info = propagate_batch(u.grid, spec, steps, src, out)
+    info = propagate_batch(u.grid, spec, steps, src, out, hist=hist)
     si = read_sysinfo(info)[:1]
     raise_on_status(si, spec)
     return Field._trusted(u.grid, out), si
@@ -259,18 +267,13 @@ def step_linear_b(u: Field, spec: PropagatorSpec) -> Field:
 def step_nonlinear(u: Field, spec: PropagatorSpec) -> tuple[Field, StepReport]:
     """One fully implicit Eyre step solved by Newton (schemes.py:270-305); the
     device records the residual norm of every Newton iteration
-    (``chp_newton_history``) for ``StepReport.residual_history``."""
+    (``chp_propagate_hist``) for ``StepReport.residual_history``."""
     import torch
     _require(spec, Scheme.NONLINEAR_EYRE)
     src = u.device_values()
-    ctx = N.Context.get(src.device.index)
     hlen = int(spec.newton_max_iter) + 1
     hist = torch.full((hlen,), float("nan"), dtype=torch.float64, device=src.device)
-    _check_ctx(ctx, ctx.L.chp_newton_history(ctx.h, N.ptr(hist), hlen), "chp_newton_history")
-    try:
-        out, si = _run_one(u, spec, 1)
-    finally:
-        ctx.L.chp_newton_history(ctx.h, None, 0)
+    out, si = _run_one(u, spec, 1, hist=hist)
     it = int(si["newton_total"][0])
     res = float(si["newton_maxres"][0])
     history = tuple(float(x) for x in hist[: it + 1].cpu().numpy())

@@ -43,7 +43,8 @@ def test_null_context_rejected():
     assert lib.chp_ctx_create(0, None) == 1
     assert lib.chp_nn_propagate(None, None, None, 1e-4, 1e-3, 1, 1, None, 0, None, 0, None, None,
                                 None, None, None) == 1
-    assert lib.chp_newton_history(None, None, 0) == 1
+    assert lib.chp_propagate_hist(None, None, None, 1, 1, None, 0, None, 0, None, None, None, 0,
+                                  None) == 1
     assert ctypes.sizeof(N.ChpNNParams) == 4 * 4 + 3 * 8
 
 

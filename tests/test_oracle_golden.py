@@ -125,3 +125,35 @@ def test_oracle_pcg_knob_matches_superlu():
         x1 = O.variable_solve(ops, a, b, v * v, rhs)
         x2 = O.variable_solve(ops, a, b, v * v, rhs, pcg=True)
         assert np.max(np.abs(x1 - x2)) / np.max(np.abs(x1)) < 1e-12
+
+
+RUN_TAGS = ("spec_pa1", "spec_pa2", "spec_pa3", "spec_npa1", "spec_npa2", "c1", "c1n", "d2", "d2n")
+
+
+def _run_case(z, tag):
+    nx, T, N, J, eps = z[f"{tag}_meta"]
+    dim = 2 if tag.startswith("d2") else 1
+    variant = {"spec_pa1": "pa1", "spec_pa2": "pa2", "spec_pa3": "pa3", "spec_npa1": "npa1",
+               "spec_npa2": "npa2", "c1": "pa3", "c1n": "npa1", "d2": "pa3", "d2n": "npa1"}[tag]
+    return O.Mesh(dim, int(nx)), variant, float(T), int(N), int(J), float(eps)
+
+
+@pytest.mark.parametrize("tag", RUN_TAGS)
+def test_oracle_serial_and_run_errors(golden, tag):
+    """a18/a19 pins: the oracle's serial fine reference equals the reference's
+    serial_fine_reference bit for bit, and its per-iteration L_inf(0,T;L2) errors
+    equal the reference run()'s records (parareal.py:145-164, 262-374)."""
+    z = golden("run_traces.npz")
+    mesh, var, T, N, J, eps = _run_case(z, tag)
+    u0 = z[f"{tag}_u0"]
+    kn = O.Knobs(cube="numpy")
+    ser = O.serial_fine(mesh, u0, var, T, N, J, eps, kn)
+    assert np.array_equal(ser, z[f"{tag}_serial"])
+    conv = int(z[f"{tag}_converged"][0])
+    r = O.parareal(mesh, u0, var, T, N, J, eps, kn, with_serial=True, inc_tol=0.0,
+                   max_iter=conv)
+    errs = np.array(r.errors)
+    want = z[f"{tag}_error"][1:]
+    assert errs.shape == want.shape
+    assert np.allclose(errs, want, rtol=1e-12, atol=1e-15), (errs, want)
+    assert errs[-1] <= 1e-6 < errs[-2]
