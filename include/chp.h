@@ -160,6 +160,17 @@ chp_status chp_max_abs_diff(chp_ctx* ctx, const chp_grid* g, int n_fields,
                             double* out, void* stream);
 
 /*
+ * chp_field_stats -- the sums behind l2_norm, energy and mass (grid.py:147-181)
+ * for n_fields fields (field f at in + f*stride), one fixed-order device
+ * reduction per field (bitwise reproducible).  out (device, 4*n_fields doubles):
+ * out[4f] = sum v^2, out[4f+1] = sum (v^2-1)^2, out[4f+2] = sum of squared
+ * differences along every axis with the Dirichlet zeros at both ends
+ * (grid.py:168-175), out[4f+3] = sum v.
+ */
+chp_status chp_field_stats(chp_ctx* ctx, const chp_grid* g, int n_fields, const double* in,
+                           long long stride, double* out, void* stream);
+
+/*
  * chp_propagate_hist -- chp_propagate that also records StepReport.residual_history
  * (schemes.py:285-290) of a NONLINEAR_EYRE propagation: for every system idx(s),
  * hist[idx * hist_len + it] = the residual norm before Newton solve `it`

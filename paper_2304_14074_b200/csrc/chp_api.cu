@@ -25,6 +25,8 @@ cudaError_t chp1d_coarse_sweep(const chp_grid& g, const chp_spec& sp, int mode, 
 cudaError_t chp_launch_max_abs_diff(const chp_grid& g, int n_fields, const double* a,
                                     long long as, const double* b, long long bs, double* out,
                                     cudaStream_t st);
+cudaError_t chp_launch_field_stats(const chp_grid& g, int n_fields, const double* in,
+                                   long long stride, double* out, cudaStream_t st);
 size_t chp_nn_scratch_bytes(int step, int nsys, int S);
 cudaError_t chp_nn_launch(const chp_grid& gr, const chp_nn_params& p, double dt, double eps2,
                           int steps, int nsys, const double* in, long long in_stride,
@@ -307,6 +309,19 @@ chp_status chp_max_abs_diff(chp_ctx* c, const chp_grid* g, int n_fields, const d
   if (n_fields == 0) return CHP_OK;
   cudaError_t e = chp_launch_max_abs_diff(*g, n_fields, a, as, b, bs, out, (cudaStream_t)stream);
   return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "max_abs_diff");
+}
+
+chp_status chp_field_stats(chp_ctx* c, const chp_grid* g, int n_fields, const double* in,
+                           long long stride, double* out, void* stream) {
+  if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  std::string why;
+  if (!grid_ok(g, &why)) return fail(c, CHP_ERR_ARG, why);
+  if (n_fields < 0 || !in || !out) return fail(c, CHP_ERR_ARG, "bad arrays");
+  if (n_fields == 0) return CHP_OK;
+  cudaError_t e = chp_launch_field_stats(*g, n_fields, in, stride, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "field_stats");
 }
 
 chp_status chp_nn_propagate(chp_ctx* c, const chp_grid* g, const chp_nn_params* nn, double dt,

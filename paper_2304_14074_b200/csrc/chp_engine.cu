@@ -35,3 +35,66 @@ cudaError_t chp_launch_max_abs_diff(const chp_grid& g, int n_fields, const doubl
   k_max_abs_diff<<<(int)blocks, 256, 0, st>>>(rows, g.m, g.pitch, n_fields, a, as, b, bs, out);
   return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// Field diagnostics (grid.py:147-181: l2_norm, energy, mass) on the device.
+// One block per field, fixed-order reduction (per-thread strided sums, then a
+// fixed shared-memory tree): bitwise reproducible.  Per field, out[4 f + q]:
+//   q = 0: sum v^2                      (l2_norm = sqrt(h^d * .))
+//   q = 1: sum (v^2 - 1)^2              (energy bulk, x 0.25)
+//   q = 2: sum of squared differences   (np.diff with the Dirichlet zeros
+//          prepended and appended along every axis, grid.py:168-175)
+//   q = 3: sum v                        (mass = h^d * .)
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kDiagThreads = 512;
+
+__global__ void __launch_bounds__(kDiagThreads) k_field_stats(int dim, int m, int pitch,
+                                                             const double* __restrict__ in,
+                                                             long long stride, double* out) {
+  __shared__ double red[4][kDiagThreads];
+  const double* v = in + (long long)blockIdx.x * stride;
+  const int off = dim == 2 ? pitch - m : 0;          // 2D rows lead with the pad column
+  const long long total = dim == 2 ? (long long)m * m : m;
+  double s2 = 0.0, sb = 0.0, sg = 0.0, s1 = 0.0;
+  for (long long t = threadIdx.x; t < total; t += kDiagThreads) {
+    const int i = dim == 2 ? (int)(t / m) : 0;
+    const int j = dim == 2 ? (int)(t % m) : (int)t;
+    const double x = v[(long long)i * pitch + off + j];
+    const double q = x * x - 1.0;
+    s2 += x * x;
+    sb += q * q;
+    s1 += x;
+    // difference with the previous node along each axis (zero before the first),
+    // plus the closing difference to the trailing zero at the last node
+    const double xl = j > 0 ? v[(long long)i * pitch + off + j - 1] : 0.0;
+    double g = (x - xl) * (x - xl);
+    if (j == m - 1) g += x * x;
+    if (dim == 2) {
+      const double xu = i > 0 ? v[(long long)(i - 1) * pitch + off + j] : 0.0;
+      g += (x - xu) * (x - xu);
+      if (i == m - 1) g += x * x;
+    }
+    sg += g;
+  }
+  red[0][threadIdx.x] = s2;
+  red[1][threadIdx.x] = sb;
+  red[2][threadIdx.x] = sg;
+  red[3][threadIdx.x] = s1;
+  __syncthreads();
+  for (int w = kDiagThreads / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w)
+      for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) out[4LL * blockIdx.x + threadIdx.x] = red[threadIdx.x][0];
+}
+
+}  // namespace
+
+cudaError_t chp_launch_field_stats(const chp_grid& g, int n_fields, const double* in,
+                                   long long stride, double* out, cudaStream_t st) {
+  k_field_stats<<<n_fields, kDiagThreads, 0, st>>>(g.dim, g.m, g.pitch, in, stride, out);
+  return cudaGetLastError();
+}

@@ -234,15 +234,52 @@ def norm_of_values(grid: SpatialGrid, values) -> float:
     return math.sqrt(grid.h ** grid.dim * float(np.dot(values, values)))
 
 
+def field_stats(grid: SpatialGrid, dev, stream=None) -> np.ndarray:
+    """Per-field sums behind l2_norm / energy / mass (grid.py:147-181), one fixed-order
+    device reduction per field (C ABI chp_field_stats).  ``dev``: CUDA float64 tensor of
+    fields in device layout (leading dims enumerate fields).  Returns [n, 4] host array:
+    sum v^2, sum (v^2-1)^2, sum of squared axis differences (Dirichlet zeros at both
+    ends), sum v."""
+    import torch
+    from . import _native as N
+    fs = grid.device_size
+    n = dev.numel() // fs
+    out = torch.empty((n, 4), dtype=torch.float64, device=dev.device)
+    ctx = N.Context.get(dev.device.index)
+    ctx.check(ctx.L.chp_field_stats(ctx.h, native_grid(grid), n, N.ptr(dev), fs, N.ptr(out),
+                                    N.stream_ptr(stream, dev.device)), "chp_field_stats")
+    return out.cpu().numpy()
+
+
+def _on_device(f: Field) -> bool:
+    return f._dev is not None and f._host is None
+
+
+def stats_l2(grid: SpatialGrid, st) -> float:
+    return math.sqrt(grid.h ** grid.dim * float(st[0]))
+
+
+def stats_energy(grid: SpatialGrid, st, eps: float) -> float:
+    return grid.h ** grid.dim * (0.25 * float(st[1]) + 0.5 * eps ** 2 * float(st[2]) / grid.h ** 2)
+
+
+def stats_mass(grid: SpatialGrid, st) -> float:
+    return grid.h ** grid.dim * float(st[3])
+
+
 def l2_norm(f: Field) -> float:
-    if f._dev is not None and f._host is None:
-        return norm_of_values(f.grid, from_device_layout(f.grid, f._dev))
+    """Cell-weighted L2 norm (grid.py:152-154); device fields reduce on the device."""
+    if _on_device(f):
+        return stats_l2(f.grid, field_stats(f.grid, f._dev)[0])
     return norm_of_values(f.grid, f.values)
 
 
 def energy(f: Field, eps: float) -> float:
-    """Discrete Ginzburg-Landau energy (grid.py:157-176)."""
+    """Discrete Ginzburg-Landau energy (grid.py:157-176); device fields reduce on the
+    device (same quadrature, fixed-order sums)."""
     g = f.grid
+    if _on_device(f):
+        return stats_energy(g, field_stats(g, f._dev)[0], eps)
     v = f.values
     bulk = 0.25 * float(np.sum((v * v - 1.0) ** 2))
     if g.dim == 1:
@@ -257,6 +294,9 @@ def energy(f: Field, eps: float) -> float:
 
 
 def mass(f: Field) -> float:
+    """h^dim * sum(u) (grid.py:179-181); device fields reduce on the device."""
+    if _on_device(f):
+        return stats_mass(f.grid, field_stats(f.grid, f._dev)[0])
     return f.grid.h ** f.grid.dim * float(np.sum(f.values))
 
 

@@ -29,7 +29,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .engine import PararealEngine
-from .grid import Field, energy, from_device_layout, l2_norm, mass
+from .grid import (Field, energy, field_stats, from_device_layout, l2_norm, mass, stats_energy,
+                   stats_l2, stats_mass)
 from .schemes import NewtonStats, PropagatorSpec, Scheme
 
 __all__ = [
@@ -199,12 +200,12 @@ def parareal_iteration(state: PararealState, variant: AlgorithmVariant,
     del workers
     Nsl = partition.num_slices
     eng = state._engine
+    fine, coarse = propagator_pair(variant, partition, eps, newton_tol=newton_tol,
+                                   newton_max_iter=newton_max_iter, nn=nn)
+    # the cached engine is reused only for exactly the specs this call would build
+    # (the reference rebuilds propagator_pair on every call, parareal.py:229-232)
     fresh = (eng is not None and eng.k == state.k and eng.N == Nsl
-             and eng.J == partition.fine_steps and eng.fine.dt == partition.fine_dt
-             and eng.fine.eps == eps and eng.fine.nn == nn
-             and eng.fine.scheme is (Scheme.NN_LINEAR_A if nn is not None else variant.fine_scheme)
-             and eng.coarse.scheme is variant.coarse_scheme
-             and eng.fine.newton_tol == newton_tol)
+             and eng.J == partition.fine_steps and eng.fine == fine and eng.coarse == coarse)
     if not fresh:
         u0 = state.iterates[0]
         eng = _engine_for(u0, variant, partition, eps, newton_tol, newton_max_iter, nn)
@@ -277,24 +278,19 @@ class RunTrace:
 
 
 def _record(eng: PararealEngine, R, eps: float, wall: float, inc=None) -> IterationRecord:
-    import torch
+    """make_record (parareal.py:342-351) on the device: the error against the serial
+    reference, the iterate norms and the tail's energy / mass come from one fixed-order
+    reduction launch over the N+1 iterates (and one over the N+1 differences)."""
     g = eng.grid
-    m = g.interior_per_axis
-    U = eng.U[0]
-    if g.dim == 2:
-        Uv = U.view(eng.N + 1, m, g.pitch)[:, :, 1:]
-        diff = (Uv - R[0].view(eng.N + 1, m, g.pitch)[:, :, 1:]) if R is not None else None
-    else:
-        Uv = U
-        diff = (U - R[0]) if R is not None else None
-    w = g.h ** g.dim
-    norms = torch.sqrt(w * (Uv * Uv).flatten(1).sum(1)).cpu().numpy()
-    err = float(torch.sqrt(w * (diff * diff).flatten(1).sum(1)).max()) if diff is not None \
-        else float("nan")
-    tail = eng.field(0, eng.N)
-    return IterationRecord(k=eng.k, error=err, energy_end=energy(tail, eps),
-                           mass_end=mass(tail), wall_seconds=wall,
-                           iterate_norms=tuple(float(x) for x in norms), increment=inc)
+    st = field_stats(g, eng.U[0])
+    norms = [stats_l2(g, st[n]) for n in range(eng.N + 1)]
+    err = float("nan")
+    if R is not None:
+        sd = field_stats(g, eng.U[0] - R[0])
+        err = max(stats_l2(g, sd[n]) for n in range(eng.N + 1))
+    return IterationRecord(k=eng.k, error=err, energy_end=stats_energy(g, st[eng.N], eps),
+                           mass_end=stats_mass(g, st[eng.N]), wall_seconds=wall,
+                           iterate_norms=tuple(norms), increment=inc)
 
 
 def run(u0: Field, variant: AlgorithmVariant, partition: TimePartition, eps: float, *,
