@@ -29,6 +29,8 @@ namespace {
 constexpr int kMinN = 8;
 constexpr int kMaxN = 1024;
 constexpr int kMaxDev = 64;
+// short row-pass strips (phase-1 row pairs per block) for small batches
+template <int N> constexpr int kStripS = linb::RowG<N>::SP >= 32 ? 8 : linb::RowG<N>::SP;
 
 // per-device one-time launch setup (function attributes, occupancy) is indexed by
 // the current device: the C ABI switches to the context's device on entry
@@ -865,13 +867,27 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
   bool& attrs = attrs_dev[cur_dev()];
   if (!attrs) {
     cudaFuncSetAttribute(linb::k2d_rowb<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
+    cudaFuncSetAttribute(linb::k2d_rowb<N, kStripS<N>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)RG::SMEM);
     cudaFuncSetAttribute(linb::k2d_colb<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
     attrs = true;
   }
   const long long fs2 = (long long)N * N;
   double* P = scratch;
   double* Qb = scratch + fs2 * nsys;
-  const dim3 rgrid((RG::NP + RG::SP - 1) / RG::SP, nsys), cgrid(N / CG::TC, nsys);
+  // strip length: the longest (fewest re-transformed halo pairs) that still gives
+  // every SM several row-pass blocks; small batches (late Parareal iterations, config
+  // 3, the serial fine reference) get short strips instead of idle SMs
+  bool short_strips = false;
+  {
+    static int sms_dev[kMaxDev] = {};
+    int& sms = sms_dev[cur_dev()];
+    if (sms == 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev());
+    short_strips = (long long)((RG::NP + RG::SP - 1) / RG::SP) * nsys < (long long)sms * RG::MINB;
+  }
+  const int strip = short_strips ? kStripS<N> : RG::SP;
+  const dim3 rgrid((RG::NP + strip - 1) / strip, nsys), cgrid(N / CG::TC, nsys);
+  auto rowb = short_strips ? linb::k2d_rowb<N, kStripS<N>> : linb::k2d_rowb<N>;
   linb::RowArgs ra{};
   ra.m = g.m; ra.cdt = sp.dt * g.c1; ra.info = info; ra.info_index = sys_index; ra.wtab = nt.wtab;
   linb::ColArgs ca{Qb, P, fs2, reinterpret_cast<const double2*>(dtab), nt.wtab};
@@ -879,12 +895,12 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
     if (s == 0) { ra.in = in; ra.in_stride = in_stride; ra.in_index = sys_index; ra.mode = linb::MODE_FIRST; }
     else { ra.in = P; ra.in_stride = fs2; ra.in_index = nullptr; ra.mode = linb::MODE_MID; }
     ra.out = Qb; ra.out_stride = fs2; ra.out_index = nullptr;
-    linb::k2d_rowb<N><<<rgrid, RG::THREADS, RG::SMEM, st>>>(ra);
+    rowb<<<rgrid, RG::THREADS, RG::SMEM, st>>>(ra);
     linb::k2d_colb<N><<<cgrid, CG::THREADS, CG::SMEM, st>>>(ca);
   }
   ra.in = P; ra.in_stride = fs2; ra.in_index = nullptr; ra.mode = linb::MODE_LAST;
   ra.out = out; ra.out_stride = out_stride; ra.out_index = sys_index;
-  linb::k2d_rowb<N><<<rgrid, RG::THREADS, RG::SMEM, st>>>(ra);
+  rowb<<<rgrid, RG::THREADS, RG::SMEM, st>>>(ra);
   return cudaGetLastError();
 }
 

@@ -51,8 +51,8 @@ template <int N> struct RowG {          // row pass geometry
   static constexpr int THREADS = WARPS * 32;
   static constexpr int G = THREADS / L;              // lane groups = row pairs per chunk
   static constexpr int NP = N / 2;                   // row pairs per field
-  static constexpr int SP = (NP < 64) ? NP : 64;     // phase-1 pairs per strip
-  static constexpr int CHUNKS = (SP + 1 + G - 1) / G;
+  static constexpr int SP = (NP < 64) ? NP : 64;     // max phase-1 pairs per strip (the
+                                                     // launch may use shorter strips: sp)
   static constexpr int SLOTS = G + 1;
   static constexpr size_t SMEM = sizeof(double2) * (size_t)SLOTS * F::RS;
   static constexpr int MINB = (N >= 1024) ? CHP_ROW_MINB : 3;
@@ -97,7 +97,9 @@ CHP_DEV void cp_wait() { asm volatile("cp.async.commit_group;\n\tcp.async.wait_g
 
 CHP_DEV double wcub(double x) { return x * fma(x, x, -3.0); }   // x^3 - 3x
 
-template <int N>
+// SPV: phase-1 row pairs per strip (compile time, so the chunk loop has a fixed trip
+// count); short strips for small batches are separate instantiations
+template <int N, int SPV = RowG<N>::SP>
 __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowArgs a) {
   using F = fdst::FG<N>;
   using RG = RowG<N>;
@@ -105,8 +107,9 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
   extern __shared__ __align__(16) double2 slots[];
   const int tid = threadIdx.x, g = tid / L, l = tid % L;
   const int sys = blockIdx.y;
-  const int sp0 = blockIdx.x * RG::SP;
-  const int sp1 = min(sp0 + RG::SP, RG::NP);           // phase-1 pairs [sp0, sp1)
+  const int sp0 = blockIdx.x * SPV;
+  const int sp1 = min(sp0 + SPV, RG::NP);              // phase-1 pairs [sp0, sp1)
+  constexpr int chunks = (SPV + 1 + G - 1) / G;
   const double2 ac = __ldg(&a.wtab[l]);
   const double sa2 = 2.0 * ac.y, ca2 = 2.0 * ac.x;
   const double2* twl = a.wtab + N + l;
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
   if (a.mode == MODE_MID) Pin = a.in + (long long)sys * a.in_stride;
   else U = a.in + (a.in_index ? (long long)a.in_index[sys] : (long long)sys) * a.in_stride;
 
-  for (int t = 0; t < RG::CHUNKS; ++t) {
+  for (int t = 0; t < chunks; ++t) {
     const int p0 = sp0 + t * G;
     // ---- phase 0: slot of pair s0 = p0 + g holds x rows (2 s0, 2 s0 + 1) ----
     {
@@ -241,35 +244,32 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
 #pragma unroll
       for (int i = 0; i < R; ++i) w0[i] = rhs[i];
       __syncwarp();
-      double2* ob = fdst::out_base<N>(r0, l);
+      // Q rows 2s1+1 (a) and 2s1+2 (b, absent for the last pair) straight from the
+      // post-processing registers: column pair k = C l + j of a row is stored at pair
+      // position pos(k) = j L + l (qpos), so the lanes of one store are contiguous
+      const int ra = 2 * s1 + 1, rb = ra + 1;
+      double* qa = Qo + (long long)(act ? ra : 0) * N;
+      double* qb = Qo + (long long)(act && rb < N ? rb : 0) * N;
+      const bool sta = act, stb = act && rb < N;
       fdst::pair_dst<N>(r0, r0, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
-        ob[2 * j] = make_double2(a0, b0);
-        ob[2 * j + 1] = make_double2(a1, b1);
+        const int pos = j * L + l;
+        if (sta) *reinterpret_cast<double2*>(qa + 2 * pos) = make_double2(a0, a1);
+        if (stb) *reinterpret_cast<double2*>(qb + 2 * pos) = make_double2(b0, b1);
       });
-      __syncwarp();
-      {
-        // rows 2s1+1 (a) and 2s1+2 (b, absent for the last pair) of Q, row-major:
-        // lane l reads (a_n, b_n), n = l + L i; even lanes store (a_n, a_{n+1}),
-        // odd lanes (b_{n-1}, b_n) after one exchange with the neighbour lane.
-        // Every lane shuffles (groups of one warp may differ in `act`).
-        const bool odd = l & 1;
-        const int ra = 2 * s1 + 1, rb = ra + 1;
-        double* rowp = Qo + (long long)(act ? (odd ? rb : ra) : 0) * N + (l & ~1);
-        const bool st = act && (!odd || rb < N);
-#pragma unroll 8
-        for (int i = 0; i < R; ++i) {
-          const double2 v = r0[l + L * i + i / Q];
-          const double o = __shfl_xor_sync(0xffffffffu, odd ? v.x : v.y, 1);
-          if (st) *reinterpret_cast<double2*>(rowp + L * i) = odd ? make_double2(o, v.y) : make_double2(v.x, o);
-        }
-      }
       __syncwarp();
     }
   }
 }
 
+// Q's column-pair order: column pair k = C l + j (row pass lane l, output j) at pair
+// position j L + l; qpos_inv maps a position back to k.
+template <int N> CHP_DEV int qpos_inv(int p) {
+  using F = fdst::FG<N>;
+  return F::C * (p % F::L) + p / F::L;
+}
+
 struct ColArgs {
-  const double* qin;       // Q (row-major, math row i at row i)
+  const double* qin;       // Q (row-major, math row i at row i, column pairs in qpos order)
   double* pout;            // P (pair-interleaved, pairs (2s, 2s+1))
   long long stride;        // doubles per system (N*N)
   const double2* dtab;     // [q/2][(2j+h) L + l]: (D''(p, q), D''(p, q+1)), p = 2(C l + j) + h
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(ColG<N>::THREADS, ColG<N>::MINB) k2d_colb(ColA
     };
     // D'' of the column pair (j0 + 2g, j0 + 2g + 1) scales the forward transform's
     // outputs in its post-processing (chunk-layout table, each value read once)
-    const double2* dr = a.dtab + (long long)(j0 / 2 + (g < GROUPS ? g : 0)) * N + l;
+    const double2* dr = a.dtab + (long long)qpos_inv<N>(j0 / 2 + (g < GROUPS ? g : 0)) * N + l;
     fdst::pair_dst<N, false, true>(reg, reg, twl, l, sa2, ca2, put, nullptr, nullptr, dr);
     __syncwarp();
     fdst::pair_dst<N>(reg, reg, twl, l, sa2, ca2, put);
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(ColG<N>::THREADS, ColG<N>::MINB) k2d_colb(ColA
       const int s = idx / GROUPS, c = idx % GROUPS;
       const double2* rg = tile + CG::RBASE(c);
       const double2 u = rg[fdst::p2<N>(2 * s)], w = rg[fdst::p2<N>(2 * s + 1)];
-      double2* dst = reinterpret_cast<double2*>(Ps + ((long long)s * N + j0 + 2 * c) * 2);
+      double2* dst = reinterpret_cast<double2*>(Ps + ((long long)s * N + 2 * qpos_inv<N>(j0 / 2 + c)) * 2);
       __stcs(dst, make_double2(u.x, w.x));
       __stcs(dst + 1, make_double2(u.y, w.y));
     }

@@ -26,26 +26,12 @@ def shard(N: int, world: int, rank: int) -> tuple[int, int]:
     return rank * L, (rank + 1) * L
 
 
-class ShardedParareal:
-    def __init__(self, grid, fine, coarse, num_slices: int, fine_steps: int, *, rank: int = 0,
-                 world: int = 1, engine_factory=None, inc_tol: float = 1e-10, device=None):
-        import torch
+class TorchComm:
+    """Point-to-point hand-off and increment reduction over torch.distributed
+    (NCCL over NVLink on the GPU box, gloo in the CPU tests)."""
+
+    def __init__(self, rank: int, world: int):
         self.rank, self.world = rank, world
-        self.N, self.J = num_slices, fine_steps
-        self.s0, self.s1 = shard(num_slices, world, rank)
-        self.local_slices = self.s1 - self.s0
-        if engine_factory is None:
-            from .engine import PararealEngine
-            engine_factory = PararealEngine
-        self.eng = engine_factory(grid, fine, coarse, self.local_slices, fine_steps, batch=1,
-                                  device=device)
-        self.grid = grid
-        self.inc_tol = inc_tol
-        self.k = 0
-        self.converged_at = None
-        self.increments = []
-        self._torch = torch
-        self._pending = []              # deferred increment reductions (iterate(defer=True))
         self._red_group = None
         if world > 1:
             # the increment all-reduce runs on its own communicator, so a deferred
@@ -54,34 +40,110 @@ class ShardedParareal:
             import torch.distributed as dist
             self._red_group = dist.new_group(list(range(world)))
 
-    # -- communication helpers ------------------------------------------------
-    def _dist(self):
+    def send(self, t, dst: int) -> None:
         import torch.distributed as dist
-        return dist
+        dist.send(t, dst=dst)
 
+    def recv(self, t, src: int) -> None:
+        import torch.distributed as dist
+        dist.recv(t, src=src)
+
+    def all_reduce_max(self, t, async_op: bool = False):
+        if self.world == 1:
+            return None
+        import torch.distributed as dist
+        return dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self._red_group, async_op=async_op)
+
+
+class LoopbackComm:
+    """Simulated ranks in one process: every shard engine lives on the
+    same device, sends are device-to-device copies into a mailbox and the increment
+    reduction is done by the driver (SimulatedRanks).  The chain runs shard after shard,
+    so no kernel ever waits on another."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.box = {}
+
+    def view(self, rank: int):
+        return _LoopbackEnd(self, rank)
+
+
+class _LoopbackEnd:
+    def __init__(self, hub: LoopbackComm, rank: int):
+        self.hub, self.rank, self.world = hub, rank, hub.world
+
+    def send(self, t, dst: int) -> None:
+        self.hub.box.setdefault((self.rank, dst), []).append(t.clone())
+
+    def recv(self, t, src: int) -> None:
+        t.copy_(self.hub.box[(src, self.rank)].pop(0))
+
+    def all_reduce_max(self, t, async_op: bool = False):
+        return None                      # SimulatedRanks reduces across shards itself
+
+
+class ShardedParareal:
+    """Parareal on one rank's contiguous slice shard, for ``batch`` independent ICs
+    (all ICs of those slices live on the rank)."""
+
+    def __init__(self, grid, fine, coarse, num_slices: int, fine_steps: int, *, rank: int = 0,
+                 world: int = 1, engine_factory=None, inc_tol: float = 1e-10, device=None,
+                 batch: int = 1, comm=None):
+        import torch
+        self.rank, self.world = rank, world
+        self.N, self.J, self.B = num_slices, fine_steps, int(batch)
+        self.s0, self.s1 = shard(num_slices, world, rank)
+        self.local_slices = self.s1 - self.s0
+        if engine_factory is None:
+            from .engine import PararealEngine
+            engine_factory = PararealEngine
+        self.eng = engine_factory(grid, fine, coarse, self.local_slices, fine_steps,
+                                  batch=self.B, device=device)
+        self.grid = grid
+        self.inc_tol = inc_tol
+        self.k = 0
+        self.converged = [None] * self.B
+        self.incs: list = []              # per-iteration [B] increments
+        self._torch = torch
+        self._pending = []              # deferred increment reductions (iterate(defer=True))
+        self.comm = comm if comm is not None else TorchComm(rank, world)
+
+    # -- batch-1 views of the reference-shaped results -------------------------
+    @property
+    def converged_at(self):
+        return self.converged[0] if self.B == 1 else self.converged
+
+    @property
+    def increments(self) -> list:
+        return [float(x[0]) for x in self.incs] if self.B == 1 else list(self.incs)
+
+    # -- communication helpers ------------------------------------------------
     def _recv_boundary(self):
-        """U_{s0} and its changed flag from rank-1 into local slot 0."""
+        """U_{s0} (all ICs) and its changed flags from rank-1 into local slot 0; the
+        local freeze bit (bit 1 of slot 0) is kept."""
         if self.rank == 0:
             return
-        dist = self._dist()
-        dist.recv(self.eng.U[0, 0], src=self.rank - 1)
-        flag = self._torch.zeros(1, dtype=self._torch.uint8, device=self.eng.U.device)
-        dist.recv(flag, src=self.rank - 1)
-        self.eng.changed[0, 0] = flag[0]
+        torch = self._torch
+        dev = self.eng.U.device
+        buf = torch.empty((self.B, self.eng.U.shape[2]), dtype=torch.float64, device=dev)
+        self.comm.recv(buf, src=self.rank - 1)
+        self.eng.U[:, 0].copy_(buf)
+        flag = torch.zeros(self.B, dtype=torch.uint8, device=dev)
+        self.comm.recv(flag, src=self.rank - 1)
+        self.eng.changed[:, 0] = (self.eng.changed[:, 0] & 2) | (flag & 1)
 
     def _send_boundary(self):
         if self.rank == self.world - 1:
             return
-        dist = self._dist()
         L = self.local_slices
-        dist.send(self.eng.U[0, L].contiguous(), dst=self.rank + 1)
-        flag = self.eng.changed[0, L:L + 1].clone()
-        dist.send(flag, dst=self.rank + 1)
+        self.comm.send(self.eng.U[:, L].contiguous(), dst=self.rank + 1)
+        self.comm.send((self.eng.changed[:, L] & 1).contiguous(), dst=self.rank + 1)
 
     # -- phases ---------------------------------------------------------------
-    def load(self, u0) -> None:
+    def load(self, u0s) -> None:
         if self.rank == 0:
-            self.eng.load([u0])
+            self.eng.load(u0s if isinstance(u0s, (list, tuple)) else [u0s])
 
     def coarse_init(self) -> None:
         self._recv_boundary()
@@ -90,19 +152,9 @@ class ShardedParareal:
         self.eng.changed.fill_(1)        # every F(U_n^0) is needed at k = 0
         self.k = 0
 
-    def iterate(self, force_all: bool = False, coarse_after=None, defer: bool = False,
-                fine_chunks=None, coarse_chunks=None, on_coarse_chunk=None):
-        """One Parareal iteration.  ``coarse_after``: an optional CUDA event the
-        coarse sweep waits for (an input copy overlapped with the fine sweep).
-        ``defer``: do not wait for the all-ranks increment (returns None; call
-        ``flush()``): rank r then starts iteration k+1 as soon as its own part of
-        the coarse chain of iteration k is done, while ranks r+1.. are still in
-        the chain (pipelined Parareal across ranks; same arithmetic).
-        ``fine_chunks``: [(lo, hi, event)] -- the fine sweep runs slice range
-        [lo, hi) after ``event`` (its inputs' copy) completes; ``coarse_chunks``:
-        [(n0, n1)] -- the coarse sweep runs in these consecutive ranges, calling
-        ``on_coarse_chunk(n0, n1)`` after each (e.g. to start copying the
-        finished iterates out).  Same arithmetic as one sweep."""
+    def fine_phase(self, force_all: bool = False, fine_chunks=None) -> None:
+        """F(U_n^k) for the local slices whose U_n changed in the last sweep (writes F
+        only: U is untouched, so this can run ahead of the increment test)."""
         eng = self.eng
         flags = eng.changed.cpu().numpy()
         if force_all:
@@ -117,14 +169,20 @@ class ShardedParareal:
                 part[:, lo:hi] = flags[:, lo:hi]
                 part[:, 0] |= flags[:, 0] & 2
                 eng.fine_sweep(part)
+
+    def coarse_phase(self, force_all: bool = False, coarse_after=None, coarse_chunks=None,
+                     on_coarse_chunk=None):
+        """The local part of the coarse chain (receive, sweep + correction, send);
+        returns the local per-IC increments (device tensor)."""
+        eng = self.eng
         if coarse_after is not None:
             self._torch.cuda.current_stream().wait_event(coarse_after)
         eng.inc.zero_()
         self._recv_boundary()
         if self.rank == 0:
-            eng.changed[0, 0] = 1 if force_all else 0
+            eng.changed[:, 0] = (eng.changed[:, 0] & 2) | (1 if force_all else 0)
         elif force_all:
-            eng.changed[0, 0] = 1
+            eng.changed[:, 0] |= 1
         if coarse_chunks is None:
             eng.coarse_range(1, 0, self.local_slices)
         else:
@@ -134,26 +192,45 @@ class ShardedParareal:
                     on_coarse_chunk(n0, n1)
         self._send_boundary()
         eng.check_status()
-        inc = eng.inc.clone()
+        return eng.inc.clone()
+
+    def iterate(self, force_all: bool = False, coarse_after=None, defer: bool = False,
+                fine_chunks=None, coarse_chunks=None, on_coarse_chunk=None):
+        """One Parareal iteration.  ``coarse_after``: an optional CUDA event the
+        coarse sweep waits for (an input copy overlapped with the fine sweep).
+        ``defer``: do not wait for the all-ranks increment (returns None; call
+        ``flush()``): rank r then starts iteration k+1 as soon as its own part of
+        the coarse chain of iteration k is done, while ranks r+1.. are still in
+        the chain (pipelined Parareal across ranks; same arithmetic).
+        ``fine_chunks``: [(lo, hi, event)] -- the fine sweep runs slice range
+        [lo, hi) after ``event`` (its inputs' copy) completes; ``coarse_chunks``:
+        [(n0, n1)] -- the coarse sweep runs in these consecutive ranges, calling
+        ``on_coarse_chunk(n0, n1)`` after each (e.g. to start copying the
+        finished iterates out).  Same arithmetic as one sweep."""
+        self.fine_phase(force_all, fine_chunks)
+        inc = self.coarse_phase(force_all, coarse_after, coarse_chunks, on_coarse_chunk)
         if defer:
-            work = None
-            if self.world > 1:
-                work = self._dist().all_reduce(inc, op=self._dist().ReduceOp.MAX,
-                                               group=self._red_group, async_op=True)
+            work = self.comm.all_reduce_max(inc, async_op=True)
             self.k += 1
             self._pending.append((self.k, work, inc))
             return None
-        if self.world > 1:
-            self._dist().all_reduce(inc, op=self._dist().ReduceOp.MAX, group=self._red_group)
+        self.comm.all_reduce_max(inc)
         self.k += 1
         return self._record(self.k, inc)
 
-    def _record(self, k, inc) -> float:
-        val = float(inc[0])
-        self.increments.append(val)
-        if self.converged_at is None and val < self.inc_tol:
-            self.converged_at = k
-        return val
+    def _record(self, k, inc):
+        """Fold the all-ranks increments of iteration k: per-IC convergence, and ICs
+        that converged are frozen on this rank (changed slot 0, bit 1)."""
+        v = inc.cpu().numpy().astype(np.float64).reshape(-1).copy()
+        for i in range(self.B):
+            if self.converged[i] is not None:
+                v[i] = 0.0
+        self.incs.append(v)
+        for i in range(self.B):
+            if self.converged[i] is None and v[i] < self.inc_tol:
+                self.converged[i] = k
+                self.eng.changed[i, 0] |= 2
+        return float(v[0]) if self.B == 1 else v
 
     def flush(self) -> None:
         """Complete the deferred increment reductions (in iteration order)."""
@@ -163,18 +240,94 @@ class ShardedParareal:
             self._record(k, inc)
         self._pending = []
 
+    def done(self) -> bool:
+        return all(c is not None for c in self.converged)
+
+    def run(self, max_iter: int | None = None, pipelined: bool = True):
+        """Coarse init, then iterate to the increment stop on every IC.  ``pipelined``:
+        the fine sweep of iteration k+1 (it writes F only) is issued before waiting for
+        the all-ranks increment of iteration k, so rank r overlaps its next fine sweep
+        with the rest of the coarse chain and the reduction; if iteration k turns out to
+        be the last, that fine sweep is discarded and the iterates are those of k.
+        Same arithmetic and stopping iteration as the synchronous loop."""
+        if max_iter is None:
+            max_iter = self.N + 2
+        self.coarse_init()
+        if not pipelined:
+            while not self.done() and self.k < max_iter:
+                self.iterate()
+            return self.converged_at
+        self.fine_phase()
+        while not self.done() and self.k < max_iter:
+            inc = self.coarse_phase()
+            work = self.comm.all_reduce_max(inc, async_op=True)
+            self.k += 1
+            if self.k < max_iter:
+                self.fine_phase()                 # speculative: U is not touched
+            if work is not None:
+                work.wait()
+            self._record(self.k, inc)
+        return self.converged_at
+
+    def local_iterates(self, i: int = 0) -> np.ndarray:
+        """Host copy of U_{s0+1} .. U_{s1} (and U_0 on rank 0) of IC i."""
+        U = self.eng.iterates_host(i)
+        return U if self.rank == 0 else U[1:]
+
+
+class SimulatedRanks:
+    """``world`` shards of one run in ONE process on one device: the
+    shard engines are the real device engines, the boundary hand-off is a
+    device-to-device copy (LoopbackComm), the coarse chain runs shard after shard and
+    the increment is the max over shards -- the sharding logic of ShardedParareal
+    exercised on one GPU, with no kernels waiting on one another."""
+
+    def __init__(self, grid, fine, coarse, num_slices: int, fine_steps: int, world: int, *,
+                 batch: int = 1, inc_tol: float = 1e-10, engine_factory=None, device=None):
+        hub = LoopbackComm(world)
+        self.shards = [ShardedParareal(grid, fine, coarse, num_slices, fine_steps, rank=r,
+                                       world=world, engine_factory=engine_factory,
+                                       inc_tol=inc_tol, device=device, batch=batch,
+                                       comm=hub.view(r))
+                       for r in range(world)]
+        self.world, self.B = world, batch
+        self.N = num_slices
+
+    def load(self, u0s) -> None:
+        self.shards[0].load(u0s)
+
+    def coarse_init(self) -> None:
+        for sh in self.shards:
+            sh.coarse_init()
+
+    def iterate(self, force_all: bool = False):
+        for sh in self.shards:
+            sh.fine_phase(force_all)
+        incs = [sh.coarse_phase(force_all) for sh in self.shards]
+        inc = incs[0]
+        for t in incs[1:]:
+            inc = self.shards[0]._torch.maximum(inc, t.to(inc.device))
+        out = None
+        for sh in self.shards:
+            sh.k += 1
+            out = sh._record(sh.k, inc)
+        return out
+
     def run(self, max_iter: int | None = None):
         if max_iter is None:
             max_iter = self.N + 2
         self.coarse_init()
-        while self.converged_at is None and self.k < max_iter:
+        sh0 = self.shards[0]
+        while not sh0.done() and sh0.k < max_iter:
             self.iterate()
-        return self.converged_at
+        return sh0.converged_at
 
-    def local_iterates(self) -> np.ndarray:
-        """Host copy of U_{s0+1} .. U_{s1} (and U_0 on rank 0)."""
-        U = self.eng.iterates_host(0)
-        return U if self.rank == 0 else U[1:]
+    @property
+    def increments(self):
+        return self.shards[0].increments
+
+    def iterates(self, i: int = 0) -> np.ndarray:
+        return np.concatenate([sh.local_iterates(i) for sh in self.shards])
 
     # -- measurement helpers (bench.py) ----------------------------------------
     def time_fine_sweep(self) -> float:
@@ -273,7 +426,8 @@ class ShardedParareal:
         ms = a.elapsed_time(b) / steps
         if self.world > 1:
             t = torch.tensor([ms], device=eng.U.device, dtype=torch.float64)
-            self._dist().all_reduce(t, op=self._dist().ReduceOp.MAX)
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         pts = self.N * self.J * self.grid.interior_count
         nbytes = eng.U.numel() * 8
