@@ -10,6 +10,14 @@ larger than L2, so no explicit flush is needed between steps.
 
 --impl reference times the reference's CPU arithmetic (the oracle port, which
 calls the same scipy SuperLU routines as the reference) on a bounded sample.
+
+Also on the line: ``time_to_tolerance`` -- full
+Parareal runs of configs 1, 2 (64 ICs) and 3 to the increment stop on the same
+GPUs in the same run (``--ttt`` selects configs; 4 and 5 take minutes), with k and
+the fine work; ``fp64`` -- a measured DFMA peak and the 1D configs' flop-model
+fractions; ``cpu_baselines`` -- the reference's arithmetic per config on this
+host's cores (config 1 in full at 1 and all workers, configs 2/3 per-step samples
+with the labelled extrapolation of SURVEY.md 8(d)); ``coarse_cg_per_step``.
 """
 
 from __future__ import annotations
@@ -199,7 +207,7 @@ def run_gpu(args):
     g = SpatialGrid(CFG["dim"], CFG["nx"])
     part = P.TimePartition(CFG["T"], CFG["N"], CFG["J"])
     fine, coarse = P.propagator_pair(P.AlgorithmVariant.PA3, part, CFG["eps"])
-    from oracle.chp_oracle import initial_condition   # seeded input generator only
+    from paper_2304_14074_b200.configs import initial_condition
     u0 = initial_condition(5)
     eng = ShardedParareal(g, fine, coarse, CFG["N"], CFG["J"], rank=rank, world=world)
     eng.load(Field(g, u0))
@@ -221,6 +229,7 @@ def run_gpu(args):
     fine_ms = eng.time_fine_sweep()
     launches, names = count_launches(step)      # every rank steps (collectives inside)
     sampler = ClockSampler(local)
+    cg0 = eng.eng.stats.coarse_cg_iterations
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -235,6 +244,7 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
+    coarse_cg = (eng.eng.stats.coarse_cg_iterations - cg0) / (args.steps * eng.local_slices)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -245,6 +255,10 @@ def run_gpu(args):
 
     # e2e: host-resident iterates through the public engine API
     e2e = eng.e2e_step_rate(args.e2e_steps) if args.e2e_steps > 0 else None
+    del eng
+    torch.cuda.empty_cache()
+    ttt = time_to_tolerance([int(c) for c in args.ttt.split(",") if c], rank, world) \
+        if args.ttt else None
 
     if rank != 0:
         if world > 1:
@@ -275,16 +289,201 @@ def run_gpu(args):
                      "kernel": "LINEAR_B fine propagator (linb::k2d_rowb + linb::k2d_colb), "
                                "32 B/grid-point-step", "traffic": traffic,
                      "traffic_unit": "DRAM bytes per grid-point-step (ncu, row+column pass)"},
+        "coarse_cg_per_step": coarse_cg,
+        "time_to_tolerance": ttt,
         "clocks": clocks, "gpu_launches": launches * args.steps if launches else launches,
         "launches_per_step": names,
         "e2e": e2e,
     }
+    line["fp64"] = fp64_block()
     if args.cpu_baseline:
         line["cpu_baseline"] = cpu_sample(args.ref_seconds)
+        line["cpu_baselines"] = cpu_baselines()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
+
+
+# ---------------------------------------------------------------------------
+# Time to tolerance, FP64 model, per-config CPU baselines
+# ---------------------------------------------------------------------------
+
+def time_to_tolerance(cfgs, rank, world) -> dict:
+    """Full Parareal runs (coarse init + iterations to max|U^{k+1}-U^k| < 1e-10, every
+    IC) of the given configs over the job's ranks (contiguous slice shards, pipelined
+    run), timed between barriers; wall = max over ranks.  Seeded inputs of SURVEY.md
+    8(d).  Fine work is the pt-steps actually computed (skip-stable slices)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_14074_b200 import parareal as P
+    from paper_2304_14074_b200.configs import CONFIGS, initial_condition
+    from paper_2304_14074_b200.distributed import ShardedParareal
+    from paper_2304_14074_b200.grid import Field, SpatialGrid
+    out = {}
+    for cfg in cfgs:
+        c = CONFIGS[cfg]
+        g = SpatialGrid(c["dim"], c["nx"])
+        B = c.get("batch", 1)
+        part = P.TimePartition(c["T"], c["N"], c["J"])
+        f, co = P.propagator_pair(P.AlgorithmVariant(c["variant"]), part, c["eps"])
+        sh = ShardedParareal(g, f, co, c["N"], c["J"], rank=rank, world=world, batch=B)
+        sh.load([Field(g, initial_condition(cfg, b)) for b in range(B)])
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sh.run(pipelined=True)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        st = sh.eng.stats
+        vals = torch.tensor([wall, float(st.fine_point_steps), float(sh.eng.newton.total_iterations),
+                             float(sh.eng.newton.steps)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            t = vals[:1].clone()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            rest = vals[1:].clone()
+            dist.all_reduce(rest, op=dist.ReduceOp.SUM)
+            vals = torch.cat([t, rest])
+        wall, fps, ntot, nsteps = (float(x) for x in vals.cpu())
+        ks = [int(k) if k is not None else None for k in sh.converged]
+        out[f"config{cfg}"] = {
+            "variant": c["variant"], "ics": B, "k": ks[0] if B == 1 else
+            {"min": min(k for k in ks if k is not None) if any(k is not None for k in ks) else None,
+             "max": max(k for k in ks if k is not None) if any(k is not None for k in ks) else None,
+             "all_converged": all(k is not None for k in ks)},
+            "seconds": wall, "fine_point_steps": fps,
+            "newton_solves_per_step": (ntot / nsteps) if nsteps else None,
+            "last_increment": float(sh.incs[-1][0]) if sh.incs else None,
+            "ranks": world}
+        del sh
+        torch.cuda.empty_cache()
+    return out
+
+
+def fp64_block() -> dict:
+    """Measured DFMA peak (chp_probe_dfma) and the 1D configs' fine propagators against
+    the flop model of BASELINE.md 3 (LINEAR_B ~21 flop/pt-step, Newton ~30 + 62 n_N)."""
+    import ctypes
+
+    import torch
+
+    from paper_2304_14074_b200 import _native as N
+    from paper_2304_14074_b200 import schemes as S
+    from paper_2304_14074_b200.configs import CONFIGS, initial_condition
+    from paper_2304_14074_b200.grid import SpatialGrid
+    ctx = N.Context.get(torch.cuda.current_device())
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    buf = torch.zeros(1, dtype=torch.float64, device="cuda")
+    blocks, iters = sms * 8, 20000
+    best = None
+    for _ in range(4):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ctx.check(ctx.L.chp_probe_dfma(ctx.h, blocks, iters, N.ptr(buf), N.stream_ptr()),
+                  "chp_probe_dfma")
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        best = ms if best is None else min(best, ms)
+    peak = 2.0 * 16 * iters * 256 * blocks / (best * 1e-3) / 1e12
+    res = {"dfma_peak_tflops": peak, "probe": f"{blocks} x 256 threads x 16 DFMA chains x {iters}"}
+
+    def rate(cfg, scheme, nsys, steps):
+        c = CONFIGS[cfg]
+        g = SpatialGrid(1, c["nx"])
+        src = torch.tensor(np.stack([initial_condition(cfg, b % 64) for b in range(nsys)]),
+                           device="cuda")
+        out = torch.empty_like(src)
+        dt = c["T"] / c["N"] / c["J"]
+        spec = S.PropagatorSpec(scheme, dt, c["eps"])
+        S.propagate_batch(g, spec, steps, src, out)
+        info = S.new_sysinfo(nsys, "cuda")
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        S.propagate_batch(g, spec, steps, src, out, info=info)
+        b.record()
+        torch.cuda.synchronize()
+        si = S.read_sysinfo(info)
+        nn = float(si["newton_total"].sum()) / max(1.0, float(si["newton_steps"].sum()))
+        return nsys * steps * g.interior_count / (a.elapsed_time(b) * 1e-3), nn
+    r1, _ = rate(1, S.Scheme.LINEAR_B, 16, 256)          # one config-1 fine sweep
+    r2, nn = rate(2, S.Scheme.NONLINEAR_EYRE, 4096, 16)  # config 2's 64 ICs x 64 slices
+    f1, f2 = 21.0, 30.0 + 62.0 * nn
+    res["config1_linear_b"] = {"pt_steps_per_s": r1, "flop_per_pt_step": f1,
+                               "tflops": r1 * f1 / 1e12, "frac": r1 * f1 / 1e12 / peak,
+                               "shape": "16 systems x 256 steps (one config-1 fine sweep)"}
+    res["config2_newton"] = {"pt_steps_per_s": r2, "newton_solves_per_step": nn,
+                             "flop_per_pt_step": f2, "tflops": r2 * f2 / 1e12,
+                             "frac": r2 * f2 / 1e12 / peak,
+                             "shape": "4096 systems x 16 steps (config 2's 64 ICs x 64 slices)"}
+    return res
+
+
+def cpu_baselines() -> dict:
+    """The reference's arithmetic per config on this host's cores (oracle port: the same
+    numpy / scipy LAPACK / SuperLU calls as the reference)."""
+    from oracle import chp_oracle as O
+    from paper_2304_14074_b200.configs import CONFIGS, initial_condition
+    cores = os.cpu_count() or 1
+    out = {"cores": cores, "kind": "port"}
+    kn = O.Knobs(cube="numpy")
+    c = CONFIGS[1]
+    m = O.Mesh(1, c["nx"])
+    u0 = initial_condition(1)
+    t0 = time.perf_counter()
+    O.serial_fine(m, u0, "pa3", c["T"], c["N"], c["J"], c["eps"], kn)
+    t_ser = time.perf_counter() - t0
+    par = {}
+    for w in (1, cores):
+        t0 = time.perf_counter()
+        r = O.parareal(m, u0, "pa3", c["T"], c["N"], c["J"], c["eps"], kn, skip_stable=False,
+                       workers=w)
+        par[w] = (time.perf_counter() - t0, r.k)
+    out["config1"] = {"serial_fine_s": t_ser, "parareal_workers1_s": par[1][0],
+                      f"parareal_workers{cores}_s": par[cores][0], "k": par[1][1],
+                      "sample": "full run (reference recomputes every slice each iteration)"}
+    # config 2: Newton fine steps of one IC; serial fine = N*J steps, Parareal (k = N+1,
+    # the reference recomputes all N slices per iteration) extrapolated from the step time
+    c = CONFIGS[2]
+    m = O.Mesh(1, c["nx"])
+    dt = c["T"] / c["N"] / c["J"]
+    t0 = time.perf_counter()
+    O.advance(m, initial_condition(2), O.EYRE, dt, c["eps"], 512, kn)
+    tf = (time.perf_counter() - t0) / 512
+    t0 = time.perf_counter()
+    O.advance(m, initial_condition(2), O.LINEAR_A, c["T"] / c["N"], c["eps"], 8, kn)
+    tg = (time.perf_counter() - t0) / 8
+    k = c["N"] + 1
+    per_ic = c["N"] * tg + k * (c["N"] * c["J"] * tf + c["N"] * tg)
+    out["config2"] = {"fine_step_ms": tf * 1e3, "coarse_step_ms": tg * 1e3,
+                      "serial_fine_per_ic_s": c["N"] * c["J"] * tf,
+                      "parareal_per_ic_s_extrapolated": per_ic,
+                      "parareal_64ics_s_extrapolated": per_ic * c["batch"] / cores,
+                      "sample": "512 Newton steps + 8 coarse steps of IC 0; T = N t_G + k (N J t_F "
+                                "+ N t_G), k = N+1, 64 ICs over the host cores"}
+    # config 3: LINEAR_B steps (cached SuperLU factor) + LINEAR_A SuperLU coarse steps
+    c = CONFIGS[3]
+    m = O.Mesh(2, c["nx"])
+    dt = c["T"] / c["N"] / c["J"]
+    u0 = initial_condition(3)
+    O.advance(m, u0, O.LINEAR_B, dt, c["eps"], 1, kn)      # factor (cached)
+    t0 = time.perf_counter()
+    O.advance(m, u0, O.LINEAR_B, dt, c["eps"], 16, kn)
+    tf = (time.perf_counter() - t0) / 16
+    t0 = time.perf_counter()
+    O.advance(m, u0, O.LINEAR_A, c["T"] / c["N"], c["eps"], 1, kn)
+    tg = time.perf_counter() - t0
+    k = 63
+    out["config3"] = {"fine_step_ms": tf * 1e3, "coarse_step_s": tg,
+                      "serial_fine_s_extrapolated": c["N"] * c["J"] * tf,
+                      "parareal_s_extrapolated": c["N"] * tg + k * (c["N"] * c["J"] * tf +
+                                                                   c["N"] * tg),
+                      "sample": "16 LINEAR_B steps + 1 SuperLU LINEAR_A step at 255^2; k = 63 "
+                                "(the GPU's and the oracle's)"}
+    return out
 
 def main():
     ap = argparse.ArgumentParser()
@@ -295,6 +494,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--ttt", default="1,2,3",
+                    help="configs whose full time to tolerance is measured (e.g. 1,2,3,4,5; '' = none)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

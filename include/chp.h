@@ -217,6 +217,11 @@ chp_status chp_nn_propagate(chp_ctx* ctx, const chp_grid* g, const chp_nn_params
                             const double* traces_in, double* traces_out,
                             chp_sys_info* info, void* stream);
 
+/* Measurement: `blocks` x 256 threads each running 16 independent DFMA chains of
+ * `iters` steps (2*16*iters flop per thread) -- the FP64 peak the 1D configs' flop
+ * model is reported against (bench.py).  `out`: one device double (scratch). */
+chp_status chp_probe_dfma(chp_ctx* ctx, int blocks, int iters, double* out, void* stream);
+
 /* Debug: barrier timestamps (globaltimer ns) of the last cooperative 2D
  * coarse sweep when CHP_COOP_TRACE is set in the environment; returns the
  * number of entries copied (0 when tracing is off). */

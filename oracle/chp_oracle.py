@@ -610,7 +610,7 @@ def coarse_start(mesh, u0, variant, T, N, eps, knobs: Knobs, counter=None):
 
 def parareal(mesh, u0, variant, T, N, J, eps, knobs: Knobs | None = None, *,
              inc_tol=1e-10, max_iter=None, keep_history=False, with_serial=False,
-             skip_stable=True, on_iteration=None):
+             skip_stable=True, on_iteration=None, workers=1):
     """Parareal to the increment test max_{n,i}|U^{k+1}-U^k| < inc_tol.
 
     The update is parareal.py:236-251 verbatim in arithmetic:
@@ -637,10 +637,19 @@ def parareal(mesh, u0, variant, T, N, J, eps, knobs: Knobs | None = None, *,
     k_done = None
     k = 0
     while k < max_iter:
-        for n in range(N):
-            if changed[n] or not skip_stable:
+        todo = [n for n in range(N) if changed[n] or not skip_stable]
+        if workers > 1:
+            # the reference's thread pool over slices (parareal.py:239-243)
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(max_workers=workers) as pool:
+                outs = list(pool.map(lambda n: fine_advance(mesh, U[n], fine, dt, eps, J, knobs,
+                                                            counter), todo))
+            for n, v in zip(todo, outs):
+                Fv[n] = v
+        else:
+            for n in todo:
                 Fv[n] = fine_advance(mesh, U[n], fine, dt, eps, J, knobs, counter)
-                fine_props += 1
+        fine_props += len(todo)
         newU = U.copy()
         new_changed = np.zeros(N + 1, bool)
         for n in range(N):

@@ -24,7 +24,7 @@ SYS_OK, SYS_NEWTON, SYS_NONFINITE, SYS_SINGULAR, SYS_CG, SYS_NN = 0, 1, 2, 3, 4,
 EXPORTS = (
     "chp_version", "chp_status_str", "chp_ctx_create", "chp_ctx_destroy", "chp_last_error",
     "chp_sysinfo_reset", "chp_propagate", "chp_coarse_sweep", "chp_max_abs_diff",
-    "chp_debug_trace", "chp_nn_propagate", "chp_propagate_hist", "chp_field_stats",
+    "chp_debug_trace", "chp_nn_propagate", "chp_propagate_hist", "chp_field_stats", "chp_probe_dfma",
 )
 
 
@@ -88,6 +88,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.chp_max_abs_diff.argtypes = [vp, C.POINTER(ChpGrid), i, vp, ll, vp, ll, vp, vp]
     L.chp_debug_trace.argtypes = [vp, i]
     L.chp_field_stats.argtypes = [vp, C.POINTER(ChpGrid), i, vp, ll, vp, vp]
+    L.chp_probe_dfma.argtypes = [vp, i, i, vp, vp]
     L.chp_propagate_hist.argtypes = [vp, C.POINTER(ChpGrid), C.POINTER(ChpSpec), i, i, vp, ll,
                                      vp, ll, vp, vp, vp, i, vp]
     L.chp_nn_propagate.argtypes = [vp, C.POINTER(ChpGrid), C.POINTER(ChpNNParams), d, d, i, i,

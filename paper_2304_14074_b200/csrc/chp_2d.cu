@@ -30,7 +30,10 @@ constexpr int kMinN = 8;
 constexpr int kMaxN = 1024;
 constexpr int kMaxDev = 64;
 // short row-pass strips (phase-1 row pairs per block) for small batches
-template <int N> constexpr int kStripS = linb::RowG<N>::SP >= 32 ? 8 : linb::RowG<N>::SP;
+// (15 + 1 = 16 phase-0 pairs: whole chunks for G <= 16 lane groups per block)
+template <int N> constexpr int kStripS = linb::RowG<N>::SP >= 32 ? 15 : linb::RowG<N>::SP;
+// (single systems, e.g. the serial fine reference: 7 + 1 = 8 phase-0 pairs)
+template <int N> constexpr int kStripT = linb::RowG<N>::SP >= 32 ? 7 : linb::RowG<N>::SP;
 
 // per-device one-time launch setup (function attributes, occupancy) is indexed by
 // the current device: the C ABI switches to the context's device on entry
@@ -487,6 +490,51 @@ __global__ void k2d_newton_commit(int nsys, const NewtonRec* rec, chp_sys_info* 
   }
 }
 
+// Newton control on the device (schemes.py:286-302), after the residual norms of
+// iteration `it`: accept at r <= tol, NewtonDivergenceError at it == max_iter or a
+// non-finite residual, otherwise stay active; the CG state follows `act`; *any is set
+// while some system still needs a solve (the host polls it, no per-system decisions).
+__global__ void k2d_newton_decide(int nsys, const double* res, int* act, int* alive, CgSys* cg,
+                                  NewtonRec* rec, int it, int max_iter, double tol, int* any) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nsys) return;
+  int a = act[s];
+  if (a) {
+    const double r = res[s];
+    NewtonRec& q = rec[s];
+    if (r <= tol) {
+      q.steps += 1;
+      q.total += it;
+      q.maxit = q.maxit > it ? q.maxit : it;
+      q.maxres = fmax(q.maxres, r);
+      a = 0;
+    } else if (it == max_iter || !isfinite(r)) {
+      if (q.status == CHP_SYS_OK) {
+        q.status = CHP_SYS_NEWTON;
+        q.fail_iter = it;
+        q.fail_res = r;
+      }
+      a = 0;
+      alive[s] = 0;
+    } else {
+      *any = 1;
+    }
+  }
+  act[s] = a;
+  cg[s].active = a; cg[s].done = 0; cg[s].fail = 0; cg[s].iters = 0;
+}
+
+// start of a step: every system that has not failed is active; first step: reset
+__global__ void k2d_newton_begin(int nsys, int* alive, int* act, NewtonRec* rec, int reset) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nsys) return;
+  if (reset) {
+    rec[s] = NewtonRec{0, 0, 0, CHP_SYS_OK, 0, 0, 0.0, 0.0};
+    alive[s] = 1;
+  }
+  act[s] = alive[s];
+}
+
 }  // namespace
 
 unsigned long long* g_coop_trace = nullptr;
@@ -512,6 +560,9 @@ struct Chp2d {
   double* pcg_tab = nullptr;      // Dk, SK (PI) for (pcg_tab_N, pcg_tab_b)
   int pcg_tab_N = 0;
   double pcg_tab_b = 0.0;
+  void* newton = nullptr;         // device Newton control: rec[n], alive[n], any flag
+  size_t newton_bytes = 0;
+  int last_cg = 8;                // CG iterations of the last batched solve (first poll)
 };
 
 Chp2d* chp2d_create() { return new Chp2d(); }
@@ -528,6 +579,7 @@ void chp2d_destroy(Chp2d* c) {
   if (c->coarse) cudaFree(c->coarse);
   if (c->pcg) cudaFree(c->pcg);
   if (c->pcg_tab) cudaFree(c->pcg_tab);
+  if (c->newton) cudaFree(c->newton);
   if (c->host_act) cudaFreeHost(c->host_act);
   if (c->host_res) cudaFreeHost(c->host_res);
   if (c->host_rec) cudaFreeHost(c->host_rec);
@@ -687,9 +739,11 @@ cudaError_t pcg_solve2(Chp2d* cx, const chp_grid& g, int nsys, double a, double 
     k_pcg2_init<N><<<eg, 256, 0, st>>>(p);
     k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 0, 0, 0, 0, 0);
   }
-  const int chunk = 8;
+  // host poll of the CG states: first after as many iterations as the last solve took
+  // (systems that finish early skip the remaining launches), then every 4
   std::vector<CgSys> host(nsys);
-  for (int it0 = 0; it0 < max_iter + chunk; it0 += chunk) {
+  int chunk = cx->last_cg < 4 ? 4 : (cx->last_cg > 32 ? 32 : cx->last_cg);
+  for (int it0 = 0; it0 < max_iter + chunk; it0 += chunk, chunk = 4) {
     for (int it = 0; it < chunk; ++it) {
       k_pcg2_rows<N, 1><<<rg, G2::THREADS, sm, st>>>(p, nullptr, p.Y, 1);
       k_pcg2_cols<N, 1><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 1);
@@ -704,8 +758,15 @@ cudaError_t pcg_solve2(Chp2d* cx, const chp_grid& g, int nsys, double a, double 
       return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     bool all = true;
-    for (int s = 0; s < nsys; ++s) all = all && (!host[s].active || host[s].done);
-    if (all) break;
+    int mx = 0;
+    for (int s = 0; s < nsys; ++s) {
+      all = all && (!host[s].active || host[s].done);
+      if (host[s].active && host[s].iters > mx) mx = host[s].iters;
+    }
+    if (all) {
+      if (mx > 0) cx->last_cg = mx;
+      break;
+    }
   }
   // x = S x^ = sigma T'_i T'_j X -> W.Yv (external layout)
   k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.X, p.Y, 0);
@@ -746,26 +807,27 @@ cudaError_t run_variable(Chp2d* cx, const chp_grid& g, const chp_spec& sp, int s
     }
     return cudaGetLastError();
   }
-  // ---- Newton (schemes.py:270-305) ----
+  // ---- Newton (schemes.py:270-305): decisions on the device, the host only polls
+  // "any system still active" once per Newton solve from the second residual on ----
   const double d = sp.dt, b = sp.b;
-  NewtonRec* rec = cx->host_rec;
-  int* hact = cx->host_act;
-  double* hres = cx->host_res;
-  for (int s = 0; s < nsys; ++s) rec[s] = NewtonRec{0, 0, 0, CHP_SYS_OK, 0, 0, 0.0, 0.0};
-  std::vector<int> alive(nsys, 1);
+  {
+    const size_t need = sizeof(NewtonRec) * nsys + sizeof(int) * (nsys + 4);
+    if ((e = grow(&cx->newton, &cx->newton_bytes, need, st)) != cudaSuccess) return e;
+  }
+  NewtonRec* drec = static_cast<NewtonRec*>(cx->newton);
+  int* alive = reinterpret_cast<int*>(drec + nsys);
+  int* any = alive + nsys;
+  int* hany = cx->host_act;                 // pinned
   for (int step = 0; step < steps; ++step) {
     const double* src = (step == 0) ? in : out;
     const long long sst = (step == 0) ? in_stride : out_stride;
     Pt pt{m, N, fs, g.c1, sys_index, sys_index};
-    for (int s = 0; s < nsys; ++s) hact[s] = alive[s];
-    cudaMemcpyAsync(W.act, hact, sizeof(int) * nsys, cudaMemcpyHostToDevice, st);
+    k2d_newton_begin<<<sb, 128, 0, st>>>(nsys, alive, W.act, drec, step == 0);
     const int alias = (src == out && sst == out_stride) ? 1 : 0;
     k2d_newton_init<<<egrid, 256, 0, st>>>(pt, src, sst, W.YH, out, out_stride, d, W.act,
                                            1 - alias);
-    std::vector<int> live = alive;
     for (int it = 0; it <= sp.newton_max_iter; ++it) {
-      for (int s = 0; s < nsys; ++s) hact[s] = live[s];
-      cudaMemcpyAsync(W.act, hact, sizeof(int) * nsys, cudaMemcpyHostToDevice, st);
+      cudaMemsetAsync(any, 0, sizeof(int), st);
       k2d_newton_t<<<egrid, 256, 0, st>>>(pt, out, out_stride, W.T1, W.T2, W.act);
       k2d_newton_h<<<egrid, 256, 0, st>>>(pt, out, out_stride, W.T1, W.T2, W.YH, W.RHS, W.Cv, b,
                                           d, W.act, W.partial + (long long)nsys * kPB * 2,
@@ -775,32 +837,13 @@ cudaError_t run_variable(Chp2d* cx, const chp_grid& g, const chp_spec& sp, int s
       if (cx->hist != nullptr && it < cx->hlen)
         k2d_newton_hist<<<sb, 128, 0, st>>>(nsys, W.res, W.act, sys_index, cx->hist, cx->hlen,
                                             it);
-      cudaMemcpyAsync(hres, W.res, sizeof(double) * nsys, cudaMemcpyDeviceToHost, st);
-      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-      bool any = false;
-      for (int s = 0; s < nsys; ++s) {
-        if (!live[s]) continue;
-        const double r = hres[s];
-        if (r <= sp.newton_tol) {
-          rec[s].steps += 1;
-          rec[s].total += it;
-          rec[s].maxit = rec[s].maxit > it ? rec[s].maxit : it;
-          rec[s].maxres = rec[s].maxres > r ? rec[s].maxres : r;
-          live[s] = 0;
-        } else if (it == sp.newton_max_iter || !std::isfinite(r)) {
-          rec[s].status = CHP_SYS_NEWTON;
-          rec[s].fail_iter = it;
-          rec[s].fail_res = r;
-          live[s] = 0;
-          alive[s] = 0;
-        } else {
-          any = true;
-        }
+      k2d_newton_decide<<<sb, 128, 0, st>>>(nsys, W.res, W.act, alive, W.cg, drec, it,
+                                            sp.newton_max_iter, sp.newton_tol, any);
+      if (it >= 1) {                        // the residual before the first solve is
+        cudaMemcpyAsync(hany, any, sizeof(int), cudaMemcpyDeviceToHost, st);   // never polled
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        if (!*hany) break;
       }
-      if (!any) break;
-      for (int s = 0; s < nsys; ++s) hact[s] = live[s];
-      cudaMemcpyAsync(W.act, hact, sizeof(int) * nsys, cudaMemcpyHostToDevice, st);
-      k2d_set_active<<<sb, 128, 0, st>>>(W.cg, nsys, W.act);
       if ((e = pcg_dispatch<N>(cx, g, nsys, 3.0 * d, b, tol, maxcg, nt, W, st,
                                step > 0 || it > 0)) != cudaSuccess)
         return e;
@@ -808,11 +851,8 @@ cudaError_t run_variable(Chp2d* cx, const chp_grid& g, const chp_spec& sp, int s
       k2d_cg_collect<<<sb, 128, 0, st>>>(nsys, W.cg, info, sys_index);
     }
   }
-  NewtonRec* drec = reinterpret_cast<NewtonRec*>(W.partial);
-  cudaMemcpyAsync(drec, rec, sizeof(NewtonRec) * nsys, cudaMemcpyHostToDevice, st);
   k2d_newton_commit<<<sb, 128, 0, st>>>(nsys, drec, info, sys_index);
-  e = cudaStreamSynchronize(st);   // rec is reused by the next call
-  return e != cudaSuccess ? e : cudaGetLastError();
+  return cudaGetLastError();
 }
 
 bool pow2_ok(const chp_grid& g, std::string* err) {
@@ -869,6 +909,8 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
     cudaFuncSetAttribute(linb::k2d_rowb<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
     cudaFuncSetAttribute(linb::k2d_rowb<N, kStripS<N>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)RG::SMEM);
+    cudaFuncSetAttribute(linb::k2d_rowb<N, kStripT<N>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)RG::SMEM);
     cudaFuncSetAttribute(linb::k2d_colb<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
     attrs = true;
   }
@@ -878,16 +920,18 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
   // strip length: the longest (fewest re-transformed halo pairs) that still gives
   // every SM several row-pass blocks; small batches (late Parareal iterations, config
   // 3, the serial fine reference) get short strips instead of idle SMs
-  bool short_strips = false;
+  bool short_strips = false, tiny_strips = false;
   {
     static int sms_dev[kMaxDev] = {};
     int& sms = sms_dev[cur_dev()];
     if (sms == 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev());
     short_strips = (long long)((RG::NP + RG::SP - 1) / RG::SP) * nsys < (long long)sms * RG::MINB;
+    tiny_strips = (long long)((RG::NP + kStripS<N> - 1) / kStripS<N>) * nsys < (long long)sms;
   }
-  const int strip = short_strips ? kStripS<N> : RG::SP;
+  const int strip = tiny_strips ? kStripT<N> : short_strips ? kStripS<N> : RG::SP;
   const dim3 rgrid((RG::NP + strip - 1) / strip, nsys), cgrid(N / CG::TC, nsys);
-  auto rowb = short_strips ? linb::k2d_rowb<N, kStripS<N>> : linb::k2d_rowb<N>;
+  auto rowb = tiny_strips ? linb::k2d_rowb<N, kStripT<N>>
+                          : short_strips ? linb::k2d_rowb<N, kStripS<N>> : linb::k2d_rowb<N>;
   linb::RowArgs ra{};
   ra.m = g.m; ra.cdt = sp.dt * g.c1; ra.info = info; ra.info_index = sys_index; ra.wtab = nt.wtab;
   linb::ColArgs ca{Qb, P, fs2, reinterpret_cast<const double2*>(dtab), nt.wtab};

@@ -27,6 +27,7 @@ cudaError_t chp_launch_max_abs_diff(const chp_grid& g, int n_fields, const doubl
                                     cudaStream_t st);
 cudaError_t chp_launch_field_stats(const chp_grid& g, int n_fields, const double* in,
                                    long long stride, double* out, cudaStream_t st);
+cudaError_t chp_launch_dfma_probe(int blocks, int iters, double* out, cudaStream_t st);
 size_t chp_nn_scratch_bytes(int step, int nsys, int S);
 cudaError_t chp_nn_launch(const chp_grid& gr, const chp_nn_params& p, double dt, double eps2,
                           int steps, int nsys, const double* in, long long in_stride,
@@ -322,6 +323,15 @@ chp_status chp_field_stats(chp_ctx* c, const chp_grid* g, int n_fields, const do
   if (n_fields == 0) return CHP_OK;
   cudaError_t e = chp_launch_field_stats(*g, n_fields, in, stride, out, (cudaStream_t)stream);
   return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "field_stats");
+}
+
+chp_status chp_probe_dfma(chp_ctx* c, int blocks, int iters, double* out, void* stream) {
+  if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  if (blocks < 1 || iters < 1 || !out) return fail(c, CHP_ERR_ARG, "bad probe arguments");
+  cudaError_t e = chp_launch_dfma_probe(blocks, iters, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "dfma probe");
 }
 
 chp_status chp_nn_propagate(chp_ctx* c, const chp_grid* g, const chp_nn_params* nn, double dt,

@@ -98,3 +98,29 @@ cudaError_t chp_launch_field_stats(const chp_grid& g, int n_fields, const double
   k_field_stats<<<n_fields, kDiagThreads, 0, st>>>(g.dim, g.m, g.pitch, in, stride, out);
   return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// FP64 peak probe (bench.py): 16 independent DFMA chains per thread, so the
+// FP64 pipe, not the dependency latency, bounds it.  2 * 16 * iters flop per thread.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(256) k_dfma_probe(int iters, double* out) {
+  double a[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = 1e-3 * (threadIdx.x + j);
+  const double m = 0.9999999, c = 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = fma(a[j], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) s += a[j];
+  if (s == 12345.678) out[0] = s;        // keeps the chains live; never true in practice
+}
+}  // namespace
+
+cudaError_t chp_launch_dfma_probe(int blocks, int iters, double* out, cudaStream_t st) {
+  k_dfma_probe<<<blocks, 256, 0, st>>>(iters, out);
+  return cudaGetLastError();
+}

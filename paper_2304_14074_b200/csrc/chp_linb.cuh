@@ -51,8 +51,9 @@ template <int N> struct RowG {          // row pass geometry
   static constexpr int THREADS = WARPS * 32;
   static constexpr int G = THREADS / L;              // lane groups = row pairs per chunk
   static constexpr int NP = N / 2;                   // row pairs per field
-  static constexpr int SP = (NP < 64) ? NP : 64;     // max phase-1 pairs per strip (the
-                                                     // launch may use shorter strips: sp)
+  // phase-1 pairs per strip: a strip of SP pairs transforms SP + 1 pairs in phase 0 in
+  // ceil((SP + 1) / G) chunks of G, so SP = 63 (64 / G chunks, 1.6 % halo overhead)
+  static constexpr int SP = (NP < 64) ? NP : 63;
   static constexpr int SLOTS = G + 1;
   static constexpr size_t SMEM = sizeof(double2) * (size_t)SLOTS * F::RS;
   static constexpr int MINB = (N >= 1024) ? CHP_ROW_MINB : 3;
@@ -96,6 +97,34 @@ CHP_DEV void cp16(void* sdst, const void* gsrc) {
 CHP_DEV void cp_wait() { asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory"); }
 
 CHP_DEV double wcub(double x) { return x * fma(x, x, -3.0); }   // x^3 - 3x
+
+// one 32-byte global store (STG.256 on sm_100)
+CHP_DEV void st256(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d) : "memory");
+}
+
+// Q's column-pair order (the row pass stores from registers, the column pass fills a
+// tile of consecutive positions): column pair k sits at pair position qpos(k).  Lane
+// l of the row pass holds k = C l + j (j < C); runs of V = min(4, C) consecutive k
+// stay adjacent and the runs of one j / V are laid out lane by lane, so a store
+// instruction covers V-pair runs of consecutive lanes, and GROUPS consecutive
+// positions of the column pass are whole runs of consecutive k (its P write-out
+// stays 128-byte coalesced).
+template <int N> struct QPos {
+  static constexpr int L = fdst::FG<N>::L, C = fdst::FG<N>::C;
+  static constexpr int V = C < 4 ? C : 4, G4 = C / V;
+};
+template <int N> CHP_DEV int qpos(int k) {
+  using QP = QPos<N>;
+  const int b = k / QP::V;
+  return QP::V * ((b % QP::G4) * QP::L + b / QP::G4) + k % QP::V;
+}
+template <int N> CHP_DEV int qpos_inv(int p) {
+  using QP = QPos<N>;
+  const int grp = p / QP::V;
+  return QP::V * ((grp % QP::L) * QP::G4 + grp / QP::L) + p % QP::V;
+}
 
 // SPV: phase-1 row pairs per strip (compile time, so the chunk loop has a fixed trip
 // count); short strips for small batches are separate instantiations
@@ -245,27 +274,25 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
       for (int i = 0; i < R; ++i) w0[i] = rhs[i];
       __syncwarp();
       // Q rows 2s1+1 (a) and 2s1+2 (b, absent for the last pair) straight from the
-      // post-processing registers: column pair k = C l + j of a row is stored at pair
-      // position pos(k) = j L + l (qpos), so the lanes of one store are contiguous
+      // post-processing registers (no staging): see qpos for the column-pair order.
+      // Consecutive outputs j, j+1 of a lane are adjacent pairs: one 32-byte store.
       const int ra = 2 * s1 + 1, rb = ra + 1;
       double* qa = Qo + (long long)(act ? ra : 0) * N;
       double* qb = Qo + (long long)(act && rb < N ? rb : 0) * N;
       const bool sta = act, stb = act && rb < N;
+      double pa0 = 0.0, pa1 = 0.0, pb0 = 0.0, pb1 = 0.0;
       fdst::pair_dst<N>(r0, r0, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
-        const int pos = j * L + l;
-        if (sta) *reinterpret_cast<double2*>(qa + 2 * pos) = make_double2(a0, a1);
-        if (stb) *reinterpret_cast<double2*>(qb + 2 * pos) = make_double2(b0, b1);
+        if ((j & 1) == 0) {
+          pa0 = a0; pa1 = a1; pb0 = b0; pb1 = b1;
+          return;
+        }
+        const int pos = qpos<N>(F::C * l + j - 1);
+        if (sta) st256(qa + 2 * pos, pa0, pa1, a0, a1);
+        if (stb) st256(qb + 2 * pos, pb0, pb1, b0, b1);
       });
       __syncwarp();
     }
   }
-}
-
-// Q's column-pair order: column pair k = C l + j (row pass lane l, output j) at pair
-// position j L + l; qpos_inv maps a position back to k.
-template <int N> CHP_DEV int qpos_inv(int p) {
-  using F = fdst::FG<N>;
-  return F::C * (p % F::L) + p / F::L;
 }
 
 struct ColArgs {

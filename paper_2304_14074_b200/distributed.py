@@ -275,6 +275,126 @@ class ShardedParareal:
         return U if self.rank == 0 else U[1:]
 
 
+    # -- measurement helpers (bench.py) ----------------------------------------
+    def time_fine_sweep(self) -> float:
+        """Device time (ms) of one fine sweep over every local slice."""
+        torch = self._torch
+        flags = np.ones((1, self.local_slices + 1), dtype=np.uint8)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        self.eng.fine_sweep(flags)
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
+    def e2e_step_rate(self, steps: int, warmup: int = 1, chunks: int = 2,
+                      coarse_chunked: bool = True) -> dict:
+        """Same metric with host-resident iterates: per step the local iterates
+        and coarse values are copied H2D from pinned memory, one forced
+        iteration runs, and the new iterates and coarse values are copied back D2H
+        (the whole PararealState round-trips through the host).  The engine state is
+        restored afterwards.  The coarse
+        values are only read by the coarse sweep, so their copy runs on a side
+        stream under the fine sweep.  The iterates move in ``chunks`` slice
+        ranges: chunk c+1 is copied in while the fine sweep of chunk c runs, and
+        the coarse sweep runs chunk by chunk with each finished range copied out
+        under the next range's sweep -- only the first chunk's input and the
+        last chunk's output copies stay exposed."""
+        torch = self._torch
+        eng = self.eng
+        hU = torch.empty(eng.U.shape, dtype=torch.float64, pin_memory=True)
+        hG = torch.empty(eng.G.shape, dtype=torch.float64, pin_memory=True)
+        hOut = torch.empty(eng.U.shape, dtype=torch.float64, pin_memory=True)
+        hGout = torch.empty(eng.G.shape, dtype=torch.float64, pin_memory=True)
+        hU.copy_(eng.U)
+        hG.copy_(eng.G)
+        saved = (eng.changed.clone(), self.k, list(self.incs), list(self.converged))
+        side = torch.cuda.Stream(device=eng.U.device)
+        h2d = torch.cuda.Stream(device=eng.U.device)
+        d2h = torch.cuda.Stream(device=eng.U.device)
+        main = torch.cuda.current_stream()
+        L = self.local_slices
+        nch = max(1, min(chunks, L))
+        bounds = [L * c // nch for c in range(nch + 1)]
+
+        def step():
+            # U^k in slice chunks on a copy stream; the fine sweep of chunk c
+            # starts when its rows have landed (chunk c+1 copies meanwhile)
+            h2d.wait_stream(main)
+            h2d.wait_stream(d2h)                      # last step's read-out of U is done
+            fine = []
+            with torch.cuda.stream(h2d):
+                for c in range(nch):
+                    lo, hi = bounds[c], bounds[c + 1]
+                    r1 = hi + 1 if c == nch - 1 else hi   # last chunk: U[L] as well
+                    eng.U[:, lo:r1].copy_(hU[:, lo:r1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(h2d)
+                    fine.append((lo, hi, ev))
+            side.wait_stream(main)                    # G is free: the last sweep is done
+            with torch.cuda.stream(side):
+                eng.G.copy_(hG, non_blocking=True)
+                g_ready = torch.cuda.Event()
+                g_ready.record(side)
+            # (the last fine chunk waits for the last copy event, so the whole of
+            # U is resident before the coarse sweep)
+
+            def out_chunk(n0, n1):
+                # U^{k+1}_{n0+1..n1} and G(U^{k+1}_{n0..n1-1}) are final: copy them out
+                # under the next chunk's coarse sweep (U_0 with the first chunk)
+                ev = torch.cuda.Event()
+                ev.record(main)
+                d2h.wait_event(ev)
+                r0 = 0 if n0 == 0 else n0 + 1
+                with torch.cuda.stream(d2h):
+                    hOut[:, r0:n1 + 1].copy_(eng.U[:, r0:n1 + 1], non_blocking=True)
+                    hGout[:, n0:n1].copy_(eng.G[:, n0:n1], non_blocking=True)
+
+            # the result U^{k+1} goes to its own buffer: every step starts from the
+            # same consistent host state (U^k, G(U^k))
+            if coarse_chunked:
+                self.iterate(force_all=True, coarse_after=g_ready, defer=True, fine_chunks=fine,
+                             coarse_chunks=[(bounds[c], bounds[c + 1]) for c in range(nch)],
+                             on_coarse_chunk=out_chunk)
+            else:
+                self.iterate(force_all=True, coarse_after=g_ready, defer=True, fine_chunks=fine)
+                out_chunk(0, L)
+
+        for _ in range(warmup):
+            step()
+        self.flush()
+        torch.cuda.synchronize()
+        assert torch.equal(hOut.to(eng.U.device), eng.U), "e2e read-out differs from U"
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            step()
+        self.flush()
+        main.wait_stream(d2h)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        # restore the engine state the measurement started from (U^k, G(U^k), k)
+        eng.U.copy_(hU)
+        eng.G.copy_(hG)
+        eng.changed.copy_(saved[0])
+        self.k, self.incs, self.converged = saved[1], saved[2], saved[3]
+        torch.cuda.synchronize()
+        if self.world > 1:
+            t = torch.tensor([ms], device=eng.U.device, dtype=torch.float64)
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        pts = self.N * self.J * self.grid.interior_count
+        nbytes = eng.U.numel() * 8
+        return {"value": pts / (ms * 1e-3), "unit": "grid-point-steps/s",
+                "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
+                "ms_per_step": ms,
+                "path": "pinned host iterates -> engine (chp_propagate/chp_coarse_sweep) -> host",
+                "copies": f"{nch} slice chunks, overlapped with the fine and coarse sweeps"}
+
+
 class SimulatedRanks:
     """``world`` shards of one run in ONE process on one device: the
     shard engines are the real device engines, the boundary hand-off is a
@@ -328,111 +448,3 @@ class SimulatedRanks:
 
     def iterates(self, i: int = 0) -> np.ndarray:
         return np.concatenate([sh.local_iterates(i) for sh in self.shards])
-
-    # -- measurement helpers (bench.py) ----------------------------------------
-    def time_fine_sweep(self) -> float:
-        """Device time (ms) of one fine sweep over every local slice."""
-        torch = self._torch
-        flags = np.ones((1, self.local_slices + 1), dtype=np.uint8)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        a.record()
-        self.eng.fine_sweep(flags)
-        b.record()
-        torch.cuda.synchronize()
-        return a.elapsed_time(b)
-
-    def e2e_step_rate(self, steps: int, warmup: int = 1, chunks: int = 2,
-                      coarse_chunked: bool = True) -> dict:
-        """Same metric with host-resident iterates: per step the local iterates
-        and coarse values are copied H2D from pinned memory, one forced
-        iteration runs, and the new iterates are copied back D2H.  The coarse
-        values are only read by the coarse sweep, so their copy runs on a side
-        stream under the fine sweep.  The iterates move in ``chunks`` slice
-        ranges: chunk c+1 is copied in while the fine sweep of chunk c runs, and
-        the coarse sweep runs chunk by chunk with each finished range copied out
-        under the next range's sweep -- only the first chunk's input and the
-        last chunk's output copies stay exposed."""
-        torch = self._torch
-        eng = self.eng
-        hU = torch.empty(eng.U.shape, dtype=torch.float64, pin_memory=True)
-        hG = torch.empty(eng.G.shape, dtype=torch.float64, pin_memory=True)
-        hOut = torch.empty(eng.U.shape, dtype=torch.float64, pin_memory=True)
-        hU.copy_(eng.U)
-        hG.copy_(eng.G)
-        side = torch.cuda.Stream(device=eng.U.device)
-        h2d = torch.cuda.Stream(device=eng.U.device)
-        d2h = torch.cuda.Stream(device=eng.U.device)
-        main = torch.cuda.current_stream()
-        L = self.local_slices
-        nch = max(1, min(chunks, L))
-        bounds = [L * c // nch for c in range(nch + 1)]
-
-        def step():
-            # U^k in slice chunks on a copy stream; the fine sweep of chunk c
-            # starts when its rows have landed (chunk c+1 copies meanwhile)
-            h2d.wait_stream(main)
-            h2d.wait_stream(d2h)                      # last step's read-out of U is done
-            fine = []
-            with torch.cuda.stream(h2d):
-                for c in range(nch):
-                    lo, hi = bounds[c], bounds[c + 1]
-                    r1 = hi + 1 if c == nch - 1 else hi   # last chunk: U[L] as well
-                    eng.U[:, lo:r1].copy_(hU[:, lo:r1], non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(h2d)
-                    fine.append((lo, hi, ev))
-            side.wait_stream(main)                    # G is free: the last sweep is done
-            with torch.cuda.stream(side):
-                eng.G.copy_(hG, non_blocking=True)
-                g_ready = torch.cuda.Event()
-                g_ready.record(side)
-            # (the last fine chunk waits for the last copy event, so the whole of
-            # U is resident before the coarse sweep)
-
-            def out_chunk(n0, n1):
-                # U^{k+1}_{n0+1..n1} are final: copy them out under the next chunk's
-                # coarse sweep (U_0 with the first chunk)
-                ev = torch.cuda.Event()
-                ev.record(main)
-                d2h.wait_event(ev)
-                r0 = 0 if n0 == 0 else n0 + 1
-                with torch.cuda.stream(d2h):
-                    hOut[:, r0:n1 + 1].copy_(eng.U[:, r0:n1 + 1], non_blocking=True)
-
-            # the result U^{k+1} goes to its own buffer: every step starts from the
-            # same consistent host state (U^k, G(U^k))
-            if coarse_chunked:
-                self.iterate(force_all=True, coarse_after=g_ready, defer=True, fine_chunks=fine,
-                             coarse_chunks=[(bounds[c], bounds[c + 1]) for c in range(nch)],
-                             on_coarse_chunk=out_chunk)
-            else:
-                self.iterate(force_all=True, coarse_after=g_ready, defer=True, fine_chunks=fine)
-                out_chunk(0, L)
-
-        for _ in range(warmup):
-            step()
-        self.flush()
-        torch.cuda.synchronize()
-        assert torch.equal(hOut.to(eng.U.device), eng.U), "e2e read-out differs from U"
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(steps):
-            step()
-        self.flush()
-        main.wait_stream(d2h)
-        b.record()
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / steps
-        if self.world > 1:
-            t = torch.tensor([ms], device=eng.U.device, dtype=torch.float64)
-            import torch.distributed as dist
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        pts = self.N * self.J * self.grid.interior_count
-        nbytes = eng.U.numel() * 8
-        return {"value": pts / (ms * 1e-3), "unit": "grid-point-steps/s",
-                "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": nbytes,
-                "ms_per_step": ms,
-                "path": "pinned host iterates -> engine (chp_propagate/chp_coarse_sweep) -> host",
-                "copies": f"{nch} slice chunks, overlapped with the fine and coarse sweeps"}

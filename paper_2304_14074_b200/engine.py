@@ -39,6 +39,8 @@ class EngineStats:
     fine_systems: int = 0          # slice-propagations actually computed
     fine_point_steps: int = 0      # grid-point-steps actually computed
     coarse_sweeps: int = 0
+    coarse_cg_iterations: int = 0  # CG iterations of the 2D LINEAR_A coarse solves (device count)
+    fine_cg_iterations: int = 0    # CG iterations of the 2D Newton / LINEAR_A fine solves
     fine_seconds: float = 0.0      # host wall time of the fine phase (synchronised)
     coarse_seconds: float = 0.0
 
@@ -188,8 +190,10 @@ class PararealEngine:
         si = self._raise(self.info_fine, self.fine, labels)
         if self.fine.scheme is Scheme.NONLINEAR_EYRE:
             self.newton.absorb(si)
+        self.stats.fine_cg_iterations += int(si["cg_total"].sum())
         self.info_fine.zero_()
         sc = self._raise(self.info_coarse, self.coarse, [f"ic {i}" for i in range(self.B)])
+        self.stats.coarse_cg_iterations += int(sc["cg_total"].sum())
         if self.coarse.scheme is Scheme.NONLINEAR_EYRE:
             self.newton.absorb(sc)
         self.info_coarse.zero_()
@@ -208,8 +212,10 @@ class PararealEngine:
         si = self._raise(self.info_fine, self.fine)
         if self.fine.scheme is Scheme.NONLINEAR_EYRE:
             self.newton.absorb(si)
+        self.stats.fine_cg_iterations += int(si["cg_total"].sum())
         self.info_fine.zero_()
         sc = self._raise(self.info_coarse, self.coarse)
+        self.stats.coarse_cg_iterations += int(sc["cg_total"].sum())
         if self.coarse.scheme is Scheme.NONLINEAR_EYRE:
             self.newton.absorb(sc)
         self.info_coarse.zero_()

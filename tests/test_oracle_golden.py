@@ -157,3 +157,13 @@ def test_oracle_serial_and_run_errors(golden, tag):
     assert errs.shape == want.shape
     assert np.allclose(errs, want, rtol=1e-12, atol=1e-15), (errs, want)
     assert errs[-1] <= 1e-6 < errs[-2]
+
+
+def test_package_configs_match_oracle_inputs():
+    """The package's seeded generators (bench / time to tolerance) produce exactly the
+    oracle's inputs, so every parity golden applies to the benchmarked workloads."""
+    from paper_2304_14074_b200 import configs as C
+    for c in range(1, 6):
+        assert C.CONFIGS[c] == O.CONFIGS[c]
+        for ic in (0, 1, 63):
+            assert np.array_equal(C.initial_condition(c, ic), O.initial_condition(c, ic))

@@ -6,7 +6,8 @@ extended-precision truth (SURVEY.md 8(c) tier T3).
   python tools/linb_truth.py cpu [tag]  -- here: the same steps in x87 long double (scipy.fft
                                            long-double DST-I, long-double stencil, cube and
                                            divisors) and in fp64 by the CPU-DST oracle and the
-                                           reference's SuperLU arithmetic (1 step);
+                                           reference's SuperLU arithmetic; writes the test
+                                           fixture tests/golden/config5_truth.npz (~30 min);
                                            prints/writes the relative max-norm errors of each
                                            against the long-double truth.
 """
@@ -75,28 +76,38 @@ def cpu(tag):
     t_truth = time.time() - t0
     res = {"grid": "1023^2", "steps": list(STEPS), "truth": "x87 long double (64-bit mantissa)",
            "truth_seconds": round(t_truth, 1)}
+    def errs(tag, k, v):
+        tr = truth[k].astype(np.float64)
+        res[f"{tag}_{k}"] = float(np.max(np.abs(v - tr)) / np.max(np.abs(tr)))
+        res[f"{tag}_{k}_sub8"] = float(np.max(np.abs(v[::8] - tr[::8])) / np.max(np.abs(tr[::8])))
+
     kn = O.Knobs(cube="numpy", spectral=True)
     o = u0
     for k in range(1, max(STEPS) + 1):
         o = O.advance(mesh, o, O.LINEAR_B, DT, EPS, 1, kn)
         if k in STEPS:
-            tr = truth[k].astype(np.float64)
-            res[f"oracle_dst_{k}"] = float(np.max(np.abs(o - tr)) / np.max(np.abs(tr)))
+            errs("oracle_dst", k, o)
     # the unmodified reference's arithmetic (SuperLU cached factor, numpy cube)
     sl = u0
     for k in range(1, max(STEPS) + 1):
         sl = O.advance(mesh, sl, O.LINEAR_B, DT, EPS, 1, O.Knobs(cube="numpy"))
         if k in STEPS:
-            tr = truth[k].astype(np.float64)
-            res[f"reference_superlu_{k}"] = float(np.max(np.abs(sl - tr)) / np.max(np.abs(tr)))
+            errs("reference_superlu", k, sl)
+    os.makedirs("gpurun_out", exist_ok=True)
     np.savez_compressed("gpurun_out/linb_truth.npz",
                         **{f"t{k}": truth[k].astype(np.float64) for k in STEPS})
+    # test fixture (tests/test_gpu_2d.py): every 8th value of the truth after 256 and
+    # 1024 steps, and the fp64 CPU paths' errors against it on the same subsample
+    fx = {f"truth{k}_sub8": truth[k].astype(np.float64)[::8].copy() for k in (256, 1024)}
+    for k in (256, 1024):
+        for tag in ("oracle_dst", "reference_superlu"):
+            fx[f"{tag}_{k}_sub8"] = np.array([res[f"{tag}_{k}_sub8"]])
+    np.savez_compressed("tests/golden/config5_truth.npz", **fx)
     f = f"gpurun_out/linb_gpu{tag}.npz"
     if os.path.exists(f):
         z = np.load(f)
         for k in STEPS:
-            tr = truth[k].astype(np.float64)
-            res[f"gpu_{k}"] = float(np.max(np.abs(z[f"s{k}"] - tr)) / np.max(np.abs(tr)))
+            errs("gpu", k, z[f"s{k}"])
     print(json.dumps(res), flush=True)
     return res
 

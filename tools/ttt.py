@@ -8,7 +8,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
-from oracle.chp_oracle import CONFIGS, initial_condition  # seeded inputs only  # noqa: E402
+from paper_2304_14074_b200.configs import CONFIGS, initial_condition  # noqa: E402
 from paper_2304_14074_b200 import parareal as P  # noqa: E402
 from paper_2304_14074_b200.engine import PararealEngine  # noqa: E402
 from paper_2304_14074_b200.grid import Field, SpatialGrid  # noqa: E402
