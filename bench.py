@@ -255,6 +255,7 @@ def run_gpu(args):
 
     # e2e: host-resident iterates through the public engine API
     e2e = eng.e2e_step_rate(args.e2e_steps) if args.e2e_steps > 0 else None
+    local_slices = eng.local_slices
     del eng
     torch.cuda.empty_cache()
     ttt = time_to_tolerance([int(c) for c in args.ttt.split(",") if c], rank, world) \
@@ -270,7 +271,7 @@ def run_gpu(args):
             traffic = json.load(f)["fine_step_bytes_per_grid_point_step"]
     except (OSError, KeyError, ValueError):
         traffic = None
-    local_pts = eng.local_slices * CFG["J"] * g.interior_count
+    local_pts = local_slices * CFG["J"] * g.interior_count
     fine_bytes = 32.0 * local_pts          # algorithmic HBM bytes of the fine sweep
     achieved = fine_bytes / (fine_ms * 1e-3) / 1e9
     line = {
