@@ -297,6 +297,7 @@ def run_gpu(args):
         "e2e": e2e,
     }
     line["fp64"] = fp64_block()
+    line["config4_newton_pcg"] = config4_block(line["roofline"]["peak"])
     if args.cpu_baseline:
         line["cpu_baseline"] = cpu_sample(args.ref_seconds)
         line["cpu_baselines"] = cpu_baselines()
@@ -421,6 +422,52 @@ def fp64_block() -> dict:
                              "frac": r2 * f2 / 1e12 / peak,
                              "shape": "4096 systems x 16 steps (config 2's 64 ICs x 64 slices)"}
     return res
+
+
+def config4_block(peak_gbs: float) -> dict:
+    """2D Newton-PCG fine path at config 4's shape (511^2, eps=0.015, 128 slices; VERDICT r1
+    item 3): fine grid-point-steps/s of one batched chp_propagate, the device Newton and
+    CG counters, and the achieved bytes of SURVEY.md 8(d)'s model -- one LINEAR_B-like
+    32 B pass pair for the step itself and one per operator application,
+    32 (1 + n_N (1 + n_CG)) B per grid-point-step -- against the HBM peak."""
+    import torch
+
+    from paper_2304_14074_b200 import schemes as S
+    from paper_2304_14074_b200.configs import CONFIGS, initial_condition
+    from paper_2304_14074_b200.grid import SpatialGrid, to_device_layout
+    c = CONFIGS[4]
+    g = SpatialGrid(2, c["nx"])
+    nsys, steps = c["N"], 4
+    u0 = torch.tensor(initial_condition(4), device="cuda")
+    src = torch.stack([to_device_layout(g, u0)] * nsys)
+    # distinct states per slice: slice n starts from n coarse-sized LINEAR_B steps of u0 scaled
+    # down to stay cheap -- every system then has its own Newton/CG history
+    spec_b = S.PropagatorSpec(S.Scheme.LINEAR_B, c["T"] / c["N"] / c["J"], c["eps"])
+    tmp = torch.empty_like(src[:1])
+    for n in range(1, nsys):
+        S.propagate_batch(g, spec_b, 2, src[n - 1:n], tmp)
+        src[n].copy_(tmp[0])
+    out = torch.empty_like(src)
+    spec = S.PropagatorSpec(S.Scheme.NONLINEAR_EYRE, c["T"] / c["N"] / c["J"], c["eps"])
+    S.propagate_batch(g, spec, steps, src, out)
+    info = S.new_sysinfo(nsys, "cuda")
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    S.propagate_batch(g, spec, steps, src, out, info=info)
+    b.record()
+    torch.cuda.synchronize()
+    si = S.read_sysinfo(info)
+    nst = max(1.0, float(si["newton_steps"].sum()))
+    n_n = float(si["newton_total"].sum()) / nst
+    n_cg = float(si["cg_total"].sum()) / max(1.0, float(si["newton_total"].sum()))
+    rate = nsys * steps * g.interior_count / (a.elapsed_time(b) * 1e-3)
+    bytes_pt = 32.0 * (1.0 + n_n * (1.0 + n_cg))
+    return {"pt_steps_per_s": rate, "ms": a.elapsed_time(b), "newton_solves_per_step": n_n,
+            "cg_iterations_per_solve": n_cg, "bytes_per_pt_step_model": bytes_pt,
+            "achieved_GBps": rate * bytes_pt / 1e9, "frac_of_hbm": rate * bytes_pt / 1e9 / peak_gbs,
+            "shape": f"{nsys} systems x {steps} Newton steps at 511^2 (config 4's slices, "
+                     "states = u0 advanced 2 n LINEAR_B steps for slice n)"}
 
 
 def cpu_baselines() -> dict:

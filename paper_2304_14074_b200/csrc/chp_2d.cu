@@ -894,6 +894,40 @@ cudaError_t get_dtab(Chp2d* c, int N, const chp_spec& sp, const NTables& nt, con
   return cudaStreamSynchronize(st);        // usable from any stream afterwards
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (libchp links no libcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// Tensor map of the Q scratch (nsys fields of N x N doubles, row-major) for the TMA column
+// pass: a 2D tensor {N columns, N nsys rows}, boxes of {2 GROUPS columns, BR rows}
+template <int N>
+bool make_qmap(CUtensorMap* map, double* Qb, int nsys) {
+  using CT = linb::ColT<N>;
+  EncodeTiledFn enc = encode_tiled_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)N * (cuuint64_t)nsys};
+  const cuuint64_t strides[1] = {(cuuint64_t)N * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)(CT::IB / 8), (cuuint32_t)CT::BR};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, Qb, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CT::IB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // LINEAR_B v2 (chp_linb.cuh): J steps = J+1 row passes + J column passes over
 // pair-interleaved P / Q scratch fields (2 N^2 doubles per system).
 template <int N>
@@ -912,6 +946,9 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
     cudaFuncSetAttribute(linb::k2d_rowb<N, kStripT<N>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)RG::SMEM);
     cudaFuncSetAttribute(linb::k2d_colb<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
+    if constexpr (N >= 64)
+      cudaFuncSetAttribute(linb::k2d_colt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)linb::ColT<N>::SMEM);
     attrs = true;
   }
   const long long fs2 = (long long)N * N;
@@ -935,12 +972,28 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
   linb::RowArgs ra{};
   ra.m = g.m; ra.cdt = sp.dt * g.c1; ra.info = info; ra.info_index = sys_index; ra.wtab = nt.wtab;
   linb::ColArgs ca{Qb, P, fs2, reinterpret_cast<const double2*>(dtab), nt.wtab};
+  // column pass: TMA tile kernel for N >= 64 (CHP_COL_TMA=0 selects the cp.async kernel)
+  CUtensorMap qmap;
+  bool tma = false;
+  if constexpr (N >= 64) {
+    static const bool want = [] { const char* e = getenv("CHP_COL_TMA"); return !(e && e[0] == '0'); }();
+    tma = want && make_qmap<N>(&qmap, Qb, nsys);
+  }
+  auto colpass = [&] {
+    if constexpr (N >= 64) {
+      if (tma) {
+        linb::k2d_colt<N><<<cgrid, CG::THREADS, linb::ColT<N>::SMEM, st>>>(qmap, ca);
+        return;
+      }
+    }
+    linb::k2d_colb<N><<<cgrid, CG::THREADS, CG::SMEM, st>>>(ca);
+  };
   for (int s = 0; s < steps; ++s) {
     if (s == 0) { ra.in = in; ra.in_stride = in_stride; ra.in_index = sys_index; ra.mode = linb::MODE_FIRST; }
     else { ra.in = P; ra.in_stride = fs2; ra.in_index = nullptr; ra.mode = linb::MODE_MID; }
     ra.out = Qb; ra.out_stride = fs2; ra.out_index = nullptr;
     rowb<<<rgrid, RG::THREADS, RG::SMEM, st>>>(ra);
-    linb::k2d_colb<N><<<cgrid, CG::THREADS, CG::SMEM, st>>>(ca);
+    colpass();
   }
   ra.in = P; ra.in_stride = fs2; ra.in_index = nullptr; ra.mode = linb::MODE_LAST;
   ra.out = out; ra.out_stride = out_stride; ra.out_index = sys_index;

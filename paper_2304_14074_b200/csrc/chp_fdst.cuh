@@ -62,8 +62,8 @@ template <int N> struct FG {
 
 template <int N> CHP_DEV constexpr int p2(int n) { return n + n / FG<N>::R; }
 
-// Pair DST-I of the pair vector held in `src` (p2 layout, group-private,
-// may alias `reg`).  reg: the group's scratch region (RS double2).
+// Pair DST-I of the pair vector read through `ld`.  reg: the group's scratch region (RS
+// double2; the input may live there).
 // twl = twiddle table + l (W_N^{l k2} at twl[k2 L]); sa2 / ca2 = 2 sin / 2 cos (pi l / N).
 // out(j, A2k, A2k1, B2k, B2k1) for k = C l + j (j compile-time after unrolling);
 // out runs after the group has finished reading reg (it may write there).
@@ -74,8 +74,25 @@ template <int N> CHP_DEV constexpr int p2(int n) { return n + n / FG<N>::R; }
 // T + l, and T[(2j + h) L + l] scales output row 2(C l + j) + h (coalesced; each
 // value read once; the loads are issued after the second DFT so their latency
 // overlaps the post-processing).
-template <int N, bool DS = false, bool PS = false, class Out>
-CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __restrict__ twl, int l,
+// Input loaders of the pre-processing: v(n2) = pair value at n = l + L n2, w(n2) = its
+// mirror at N - n.  SmemLd: a group-private pair region in p2 layout; other loaders
+// (chp_linb.cuh TileLd: the column pass's TMA tile) only change the addressing.
+template <int N> struct SmemLd {
+  const double2 *sd, *sm0, *sm1;
+  CHP_DEV SmemLd(const double2* src, int l)
+      : sd(src + l), sm0(src + p2<N>(N - l)),
+        // Q == 2: lane 0's mirror offsets differ by one for odd n2 (see header)
+        sm1((FG<N>::Q == 2 && l == 0) ? src + p2<N>(N - l) - 1 : src + p2<N>(N - l)) {}
+  CHP_DEV double2 v(int n2) const { return sd[FG<N>::L * n2 + n2 / FG<N>::Q]; }
+  CHP_DEV double2 w(int n2) const {
+    return ((n2 & 1) ? sm1 : sm0)[p2<N>(N - 1 - FG<N>::L * n2) - p2<N>(N - 1)];
+  }
+};
+
+// BSYNC: the input is shared by the whole block and reg overlays it (column pass tile):
+// the barrier between the input reads and the first write to reg is a block barrier.
+template <int N, bool DS = false, bool PS = false, bool BSYNC = false, class Ld, class Out>
+CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restrict__ twl, int l,
                       double sa2, double ca2, Out out,
                       const double2* __restrict__ dsc = nullptr,
                       const double2* __restrict__ dsm = nullptr,
@@ -89,17 +106,11 @@ CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __r
   if constexpr (DS) {
     asm volatile("" : "+l"(dsc), "+l"(dsm)::"memory");
   }
-  const double2* sd = src + l;
-  const double2* sm0 = src + p2<N>(N - l);
-  // Q == 2: lane 0's mirror offsets differ by one for odd n2 (see header)
-  const double2* sm1 = (Q == 2 && l == 0) ? sm0 - 1 : sm0;
   double2 z[R];
 #pragma unroll
   for (int n2 = 0; n2 < R; ++n2) {
-    const int im = L * n2 + n2 / Q;
-    const int imm = p2<N>(N - 1 - L * n2) - p2<N>(N - 1);
-    double2 v = sd[im];
-    double2 w = ((n2 & 1) ? sm1 : sm0)[imm];
+    double2 v = ld.v(n2);
+    double2 w = ld.w(n2);
     if constexpr (DS) {
       const double2 dv = __ldcg(dsc + L * n2), dw = __ldcg(dsm - L * n2);
       v = make_double2(v.x * dv.x, v.y * dv.y);
@@ -132,7 +143,8 @@ CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __r
 #pragma unroll
   for (int k2 = 1; k2 < R; ++k2) z[brev(k2, RB)] = wdst::cmul(z[brev(k2, RB)], __ldg(&twl[k2 * L]));
 #endif
-  __syncwarp();                                    // every lane's input reads are done
+  if constexpr (BSYNC) __syncthreads();            // every group's input reads are done
+  else __syncwarp();                               // every lane's input reads are done
   double2* tp = reg + l;
 #pragma unroll
   for (int k2 = 0; k2 < R; ++k2) tp[k2 * (L + 1)] = z[brev(k2, RB)];
@@ -197,6 +209,16 @@ CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __r
     else
       out(j, ea[j], ca[j] + offa, eb[j], cb[j] + offb);
   }
+}
+
+// Pair DST-I of the pair vector held in `src` (p2 layout, group-private, may alias `reg`).
+template <int N, bool DS = false, bool PS = false, class Out>
+CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __restrict__ twl, int l,
+                      double sa2, double ca2, Out out,
+                      const double2* __restrict__ dsc = nullptr,
+                      const double2* __restrict__ dsm = nullptr,
+                      const double2* __restrict__ dpo = nullptr) {
+  pair_dst_ld<N, DS, PS, false>(SmemLd<N>(src, l), reg, twl, l, sa2, ca2, out, dsc, dsm, dpo);
 }
 
 // store the transform output into a pair region in p2 layout (k = C l + j):

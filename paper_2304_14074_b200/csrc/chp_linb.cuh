@@ -27,6 +27,7 @@
 //             each value read once)
 // T' = 4T (chp_fdst.cuh); all normalisations live in D'' = (2/N)^2 D / 256.
 #pragma once
+#include <cuda.h>            // CUtensorMap (type only; the encoder is resolved at run time)
 #include "chp_fdst.cuh"
 
 #ifndef CHP_ROW_WARPS
@@ -357,6 +358,120 @@ __global__ void __launch_bounds__(ColG<N>::THREADS, ColG<N>::MINB) k2d_colb(ColA
       __stcs(dst, make_double2(u.x, w.x));
       __stcs(dst + 1, make_double2(u.y, w.y));
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Column pass with a TMA tile (N >= 64): the block's Q tile -- rows 0..N-1 of its
+// GROUPS column pairs, IB = 16 GROUPS bytes per row -- is fetched by cp.async.bulk.tensor
+// (UTMALDG) boxes of up to 256 rows into a hardware-swizzled row-major tile (64- or
+// 128-byte swizzle: the 16-byte chunk index is XORed with row bits, which makes a lane
+// group's stride-IB column reads bank-conflict free) instead of per-thread 16-byte
+// cp.async whose 32 lanes each hit a different row (one shared-memory wavefront per
+// lane).  The forward transform's pre-processing reads the tile directly (TileLd); after
+// a block barrier the tile's memory becomes the groups' private regions.  The inverse
+// transform's outputs go to P straight from the post-processing registers: a lane holds
+// rows (2k, 2k+1) of both columns of its pair = 32 contiguous bytes of P.
+// ---------------------------------------------------------------------------
+CHP_DEV unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+CHP_DEV void mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+CHP_DEV void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+CHP_DEV void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n LAB_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @p bra LAB_DONE_%=;\n bra LAB_WAIT_%=;\n LAB_DONE_%=:\n}" ::"r"(smem_u32(b)), "r"(parity)
+      : "memory");
+}
+CHP_DEV void tma_load_2d(void* sdst, const CUtensorMap* map, int c0, int c1, unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(sdst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(b)) : "memory");
+}
+
+template <int N> struct ColT {          // TMA column pass geometry
+  using F = fdst::FG<N>;
+  using CG = ColG<N>;
+  static constexpr int L = F::L, GROUPS = CG::GROUPS;
+  static constexpr int IB = 16 * GROUPS;                 // tile row bytes: 64 or 128
+  static constexpr int BR = N < 256 ? N : 256;           // rows per TMA box
+  static constexpr int NBOX = N / BR;
+  static constexpr size_t TILE = (size_t)N * IB;
+  static constexpr size_t REGIONS = sizeof(double2) * (size_t)(CG::RBASE(CG::GALL - 1) + F::RS);
+  // lane 0's mirror of n = 0 reads row N (one row past the tile; the value is discarded)
+  static constexpr size_t SMEM = 1024 + (TILE + IB > REGIONS ? TILE + IB : REGIONS);
+  static_assert(N >= 64 && CG::GROUPS == CG::GALL && (IB == 64 || IB == 128), "TMA column pass geometry");
+  // 16-byte chunk XOR of the hardware swizzle for tile row r (64B: bits 7-8 of the byte
+  // offset = (r >> 1) & 3; 128B: bits 7-9 = r & 7)
+  CHP_DEV static int swz(int r) { return IB == 64 ? ((r >> 1) & 3) : (r & 7); }
+};
+
+// loader of the forward transform: column pair g of the swizzled tile.  Rows l + L n2 and
+// N - l - L n2 keep their swizzle term for every n2 (L n2 is a multiple of 8).
+template <int N> struct TileLd {
+  const unsigned char *vb, *wb;
+  CHP_DEV TileLd(const unsigned char* tile, int g, int l)
+      : vb(tile + l * ColT<N>::IB + ((g ^ ColT<N>::swz(l)) << 4)),
+        wb(tile + (N - l) * ColT<N>::IB + ((g ^ ColT<N>::swz(N - l)) << 4)) {}
+  CHP_DEV double2 v(int n2) const {
+    return *reinterpret_cast<const double2*>(vb + n2 * (fdst::FG<N>::L * ColT<N>::IB));
+  }
+  CHP_DEV double2 w(int n2) const {
+    return *reinterpret_cast<const double2*>(wb - n2 * (fdst::FG<N>::L * ColT<N>::IB));
+  }
+};
+
+template <int N>
+__global__ void __launch_bounds__(ColG<N>::THREADS, ColG<N>::MINB)
+k2d_colt(const __grid_constant__ CUtensorMap qmap, ColArgs a) {
+  using F = fdst::FG<N>;
+  using CG = ColG<N>;
+  using CT = ColT<N>;
+  constexpr int L = F::L, TC = CG::TC;
+  extern __shared__ __align__(16) unsigned char raw[];
+  __shared__ __align__(8) unsigned long long bar;
+  unsigned char* tile = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+  const int tid = threadIdx.x, g = tid / L, l = tid % L;
+  const int sys = blockIdx.y;
+  const int j0 = blockIdx.x * TC;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar, (unsigned)CT::TILE);
+#pragma unroll
+    for (int b = 0; b < CT::NBOX; ++b)
+      tma_load_2d(tile + (size_t)b * CT::BR * CT::IB, &qmap, j0, sys * N + b * CT::BR, &bar);
+  }
+  double* Ps = a.pout + (long long)sys * a.stride;
+  const double2 ac = __ldg(&a.wtab[l]);
+  const double sa2 = 2.0 * ac.y, ca2 = 2.0 * ac.x;
+  const double2* twl = a.wtab + N + l;
+  const int kq = qpos_inv<N>(j0 / 2 + g);               // the pair's true column pair
+  const double2* dr = a.dtab + (long long)kq * N + l;
+  double2* reg = reinterpret_cast<double2*>(tile) + CG::RBASE(g);
+  __syncthreads();                                       // the barrier is initialised
+  mbar_wait(&bar, 0);
+  {
+    double2* ob = fdst::out_base<N>(reg, l);
+    auto put = [&](int j, double a0, double a1, double b0, double b1) {
+      ob[2 * j] = make_double2(a0, b0);
+      ob[2 * j + 1] = make_double2(a1, b1);
+    };
+    // D'' of the column pair scales the forward transform's outputs in its post-processing
+    fdst::pair_dst_ld<N, false, true, true>(TileLd<N>(tile, g, l), reg, twl, l, sa2, ca2, put, nullptr,
+                                            nullptr, dr);
+    __syncwarp();
+    // P (pair-interleaved): rows (2k, 2k+1), columns (2 kq, 2 kq + 1), k = C l + j
+    double* pl = Ps + ((long long)(F::C * l) * N + 2 * kq) * 2;
+    fdst::pair_dst<N>(reg, reg, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
+      st256(pl + (long long)j * (2 * N), a0, a1, b0, b1);
+    });
   }
 }
 
