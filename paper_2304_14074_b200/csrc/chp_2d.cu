@@ -928,6 +928,23 @@ bool make_qmap(CUtensorMap* map, double* Qb, int nsys) {
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Tensor map of the P scratch for the column pass's TMA store (N = 1024): a row pair is 2N
+// doubles; dimension order {columns, l, j} with row pair k = C l + j (chp_linb.cuh ColT)
+template <int N>
+bool make_pmap(CUtensorMap* map, double* P, int nsys) {
+  using F = fdst::FG<N>;
+  EncodeTiledFn enc = encode_tiled_fn();
+  if (!enc) return false;
+  const cuuint64_t rp = (cuuint64_t)2 * N * sizeof(double);   // bytes per row pair
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * N, (cuuint64_t)F::L * (cuuint64_t)nsys, (cuuint64_t)F::C};
+  const cuuint64_t strides[2] = {rp * F::C, rp};
+  const cuuint32_t box[3] = {16, (cuuint32_t)F::L, (cuuint32_t)F::C};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, P, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // LINEAR_B v2 (chp_linb.cuh): J steps = J+1 row passes + J column passes over
 // pair-interleaved P / Q scratch fields (2 N^2 doubles per system).
 template <int N>
@@ -973,16 +990,18 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
   ra.m = g.m; ra.cdt = sp.dt * g.c1; ra.info = info; ra.info_index = sys_index; ra.wtab = nt.wtab;
   linb::ColArgs ca{Qb, P, fs2, reinterpret_cast<const double2*>(dtab), nt.wtab};
   // column pass: TMA tile kernel for N >= 64 (CHP_COL_TMA=0 selects the cp.async kernel)
-  CUtensorMap qmap;
+  CUtensorMap qmap, pmap;
   bool tma = false;
   if constexpr (N >= 64) {
     static const bool want = [] { const char* e = getenv("CHP_COL_TMA"); return !(e && e[0] == '0'); }();
     tma = want && make_qmap<N>(&qmap, Qb, nsys);
+    if (tma && linb::ColT<N>::PSTORE) tma = make_pmap<N>(&pmap, P, nsys);
+    else if (tma) pmap = qmap;
   }
   auto colpass = [&] {
     if constexpr (N >= 64) {
       if (tma) {
-        linb::k2d_colt<N><<<cgrid, CG::THREADS, linb::ColT<N>::SMEM, st>>>(qmap, ca);
+        linb::k2d_colt<N><<<cgrid, CG::THREADS, linb::ColT<N>::SMEM, st>>>(qmap, pmap, ca);
         return;
       }
     }

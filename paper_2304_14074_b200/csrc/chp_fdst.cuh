@@ -91,7 +91,9 @@ template <int N> struct SmemLd {
 
 // BSYNC: the input is shared by the whole block and reg overlays it (column pass tile):
 // the barrier between the input reads and the first write to reg is a block barrier.
-template <int N, bool DS = false, bool PS = false, bool BSYNC = false, class Ld, class Out>
+// OSYNC: out() writes memory that other groups' regions overlay (the column pass's P tile):
+// the barrier between the last read of reg and out() is a block barrier.
+template <int N, bool DS = false, bool PS = false, bool BSYNC = false, bool OSYNC = false, class Ld, class Out>
 CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restrict__ twl, int l,
                       double sa2, double ca2, Out out,
                       const double2* __restrict__ dsc = nullptr,
@@ -200,7 +202,8 @@ CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restr
     if (l >= o) { ia += ya; ib += yb; }
   }
   const double offa = ia - sa, offb = ib - sb;
-  __syncwarp();                                    // Z reads done before out() writes reg
+  if constexpr (OSYNC) __syncthreads();            // every group's Z reads are done
+  else __syncwarp();                               // Z reads done before out() writes reg
 #pragma unroll
   for (int j = 0; j < C; ++j) {
     if constexpr (PS)
@@ -218,7 +221,7 @@ CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __r
                       const double2* __restrict__ dsc = nullptr,
                       const double2* __restrict__ dsm = nullptr,
                       const double2* __restrict__ dpo = nullptr) {
-  pair_dst_ld<N, DS, PS, false>(SmemLd<N>(src, l), reg, twl, l, sa2, ca2, out, dsc, dsm, dpo);
+  pair_dst_ld<N, DS, PS, false, false>(SmemLd<N>(src, l), reg, twl, l, sa2, ca2, out, dsc, dsm, dpo);
 }
 
 // store the transform output into a pair region in p2 layout (k = C l + j):

@@ -97,6 +97,43 @@ CHP_DEV void cp16(void* sdst, const void* gsrc) {
 }
 CHP_DEV void cp_wait() { asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory"); }
 
+CHP_DEV unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+CHP_DEV void mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+CHP_DEV void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+CHP_DEV void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n LAB_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @p bra LAB_DONE_%=;\n bra LAB_WAIT_%=;\n LAB_DONE_%=:\n}" ::"r"(smem_u32(b)), "r"(parity)
+      : "memory");
+}
+CHP_DEV void tma_load_2d(void* sdst, const CUtensorMap* map, int c0, int c1, unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(sdst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(b)) : "memory");
+}
+
+// one contiguous global -> shared bulk copy (UBLKCP), completion on an mbarrier
+CHP_DEV void bulk_load(void* sdst, const void* gsrc, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+CHP_DEV void fence_async_proxy() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// loader of a transform whose input is an unpadded pair vector (a row pair as the bulk
+// copy lands it): v = src[l + L n2], mirror src[N - l - L n2] (src[N] for n = 0: discarded)
+template <int N> struct PlainLd {
+  const double2 *vb, *wb;
+  CHP_DEV PlainLd(const double2* src, int l) : vb(src + l), wb(src + N - l) {}
+  CHP_DEV double2 v(int n2) const { return vb[fdst::FG<N>::L * n2]; }
+  CHP_DEV double2 w(int n2) const { return wb[-fdst::FG<N>::L * n2]; }
+};
+
 CHP_DEV double wcub(double x) { return x * fma(x, x, -3.0); }   // x^3 - 3x
 
 // one 32-byte global store (STG.256 on sm_100)
@@ -145,6 +182,21 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
   const double2* twl = a.wtab + N + l;
   const int m = a.m;
   const double cdt = a.cdt;
+  // MODE_MID, one warp per pair (N = 1024): each group's row pair arrives by one bulk copy
+  // (UBLKCP) on the group's mbarrier; narrower groups (two or more per warp, 4 KB pairs or
+  // less) keep the per-thread cp.async fill, which measured faster there
+  constexpr bool BULK = (L == 32);
+  __shared__ __align__(8) unsigned long long rbar[G];
+  unsigned rphase = 0;
+  if (BULK && a.mode == MODE_MID) {
+    if (tid == 0) {
+#pragma unroll
+      for (int i = 0; i < G; ++i) mbar_init(&rbar[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      fence_async_proxy();
+    }
+    __syncthreads();
+  }
 
   if (a.mode == MODE_LAST) {
     // x = T' P for pairs [sp0, sp1) -> physical rows (2s, 2s+1) = storage rows 2s-1, 2s
@@ -202,18 +254,29 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
       double2* reg = slots + ((t * G + g) % SL) * RS;
       const bool load = s0 <= sp1 && s0 < RG::NP;
       if (a.mode == MODE_MID) {
-        const double2* src = reinterpret_cast<const double2*>(Pin + (long long)(load ? s0 : 0) * 2 * N);
+        // the copy of chunk t > 0 was issued from the previous chunk's phase 1 (below)
         if (load) {
+          if constexpr (BULK) {
+            if (t == 0 && l == 0) {
+              mbar_expect_tx(&rbar[g], 16u * N);
+              bulk_load(reg, Pin + (long long)s0 * 2 * N, 16u * N, &rbar[g]);
+            }
+            mbar_wait(&rbar[g], rphase);
+            rphase ^= 1;
+          } else {
+            const double2* src = reinterpret_cast<const double2*>(Pin + (long long)s0 * 2 * N);
 #pragma unroll 4
-          for (int i = 0; i < R; ++i) cp16(&reg[l + L * i + i / Q], &src[l + L * i]);
+            for (int i = 0; i < R; ++i) cp16(&reg[l + L * i], &src[l + L * i]);
+            cp_wait();
+          }
         } else {
 #pragma unroll 4
-          for (int i = 0; i < R; ++i) reg[l + L * i + i / Q] = make_double2(0.0, 0.0);
+          for (int i = 0; i < R; ++i) reg[l + L * i] = make_double2(0.0, 0.0);
         }
-        cp_wait();
         __syncwarp();
         double2* ob = fdst::out_base<N>(reg, l);
-        fdst::pair_dst<N>(reg, reg, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
+        fdst::pair_dst_ld<N>(PlainLd<N>(reg, l), reg, twl, l, sa2, ca2,
+                             [&](int j, double a0, double a1, double b0, double b1) {
           ob[2 * j] = make_double2(a0, b0);
           ob[2 * j + 1] = make_double2(a1, b1);
         });
@@ -282,8 +345,17 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
       double* qb = Qo + (long long)(act && rb < N ? rb : 0) * N;
       const bool sta = act, stb = act && rb < N;
       double pa0 = 0.0, pa1 = 0.0, pb0 = 0.0, pb1 = 0.0;
+      // r0 is this group's phase-0 slot of the next chunk: its row pair is requested as soon
+      // as the transform has read its last value from the slot (the callbacks run after that)
+      const int sn = p0 + G + g;
+      const bool prefetch = BULK && a.mode == MODE_MID && t + 1 < chunks && sn <= sp1 && sn < RG::NP;
       fdst::pair_dst<N>(r0, r0, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
         if ((j & 1) == 0) {
+          if (j == 0 && prefetch && l == 0) {
+            fence_async_proxy();
+            mbar_expect_tx(&rbar[g], 16u * N);
+            bulk_load(r0, Pin + (long long)sn * 2 * N, 16u * N, &rbar[g]);
+          }
           pa0 = a0; pa1 = a1; pb0 = b0; pb1 = b1;
           return;
         }
@@ -373,25 +445,12 @@ __global__ void __launch_bounds__(ColG<N>::THREADS, ColG<N>::MINB) k2d_colb(ColA
 // transform's outputs go to P straight from the post-processing registers: a lane holds
 // rows (2k, 2k+1) of both columns of its pair = 32 contiguous bytes of P.
 // ---------------------------------------------------------------------------
-CHP_DEV unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
-CHP_DEV void mbar_init(unsigned long long* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+CHP_DEV void tma_store_3d(const CUtensorMap* map, const void* ssrc, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+               ::"l"(map), "r"(smem_u32(ssrc)), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
-CHP_DEV void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-               : "memory");
-}
-CHP_DEV void mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n LAB_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @p bra LAB_DONE_%=;\n bra LAB_WAIT_%=;\n LAB_DONE_%=:\n}" ::"r"(smem_u32(b)), "r"(parity)
-      : "memory");
-}
-CHP_DEV void tma_load_2d(void* sdst, const CUtensorMap* map, int c0, int c1, unsigned long long* b) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(smem_u32(sdst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(b)) : "memory");
+CHP_DEV void tma_store_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\n\tcp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 template <int N> struct ColT {          // TMA column pass geometry
@@ -409,6 +468,13 @@ template <int N> struct ColT {          // TMA column pass geometry
   // 16-byte chunk XOR of the hardware swizzle for tile row r (64B: bits 7-8 of the byte
   // offset = (r >> 1) & 3; 128B: bits 7-9 = r & 7)
   CHP_DEV static int swz(int r) { return IB == 64 ? ((r >> 1) & 3) : (r & 7); }
+  // P leaves through one TMA store (UTMASTG) when the block's pairs span 128 bytes of a P
+  // row pair (GROUPS = 4: N = 1024): the inverse transform's outputs are staged in a
+  // 128-byte-swizzled tile [j][l][128 B] (row pair k = C l + j at tile row j L + l, so the
+  // 32 lanes of a store instruction hit 32 consecutive tile rows: conflict free), and the
+  // tensor map's dimension order {columns, l, j} scatters the tile rows to P's row pairs
+  static constexpr bool PSTORE = (GROUPS == 4);
+  static constexpr size_t PTILE = (size_t)(N / 2) * 128;
 };
 
 // loader of the forward transform: column pair g of the swizzled tile.  Rows l + L n2 and
@@ -428,7 +494,7 @@ template <int N> struct TileLd {
 
 template <int N>
 __global__ void __launch_bounds__(ColG<N>::THREADS, ColG<N>::MINB)
-k2d_colt(const __grid_constant__ CUtensorMap qmap, ColArgs a) {
+k2d_colt(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap pmap, ColArgs a) {
   using F = fdst::FG<N>;
   using CG = ColG<N>;
   using CT = ColT<N>;
@@ -468,10 +534,28 @@ k2d_colt(const __grid_constant__ CUtensorMap qmap, ColArgs a) {
                                             nullptr, dr);
     __syncwarp();
     // P (pair-interleaved): rows (2k, 2k+1), columns (2 kq, 2 kq + 1), k = C l + j
-    double* pl = Ps + ((long long)(F::C * l) * N + 2 * kq) * 2;
-    fdst::pair_dst<N>(reg, reg, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
-      st256(pl + (long long)j * (2 * N), a0, a1, b0, b1);
-    });
+    if constexpr (CT::PSTORE) {
+      // tile row j L + l, 16-byte chunks 2g and 2g + 1, XOR-swizzled with the row's low bits
+      unsigned char* pt = tile + l * 128;
+      const int c0 = ((2 * g) ^ (l & 7)) << 4, c1 = ((2 * g + 1) ^ (l & 7)) << 4;
+      fdst::pair_dst_ld<N, false, false, false, true>(
+          fdst::SmemLd<N>(reg, l), reg, twl, l, sa2, ca2,
+          [&](int j, double a0, double a1, double b0, double b1) {
+            *reinterpret_cast<double2*>(pt + j * (L * 128) + c0) = make_double2(a0, a1);
+            *reinterpret_cast<double2*>(pt + j * (L * 128) + c1) = make_double2(b0, b1);
+          });
+      fence_async_proxy();
+      __syncthreads();
+      if (tid == 0) {
+        tma_store_3d(&pmap, tile, 4 * qpos_inv<N>(j0 / 2), sys * L, 0);
+        tma_store_commit_wait_read();
+      }
+    } else {
+      double* pl = Ps + ((long long)(F::C * l) * N + 2 * kq) * 2;
+      fdst::pair_dst<N>(reg, reg, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
+        st256(pl + (long long)j * (2 * N), a0, a1, b0, b1);
+      });
+    }
   }
 }
 
