@@ -966,6 +966,9 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
     if constexpr (N >= 64)
       cudaFuncSetAttribute(linb::k2d_colt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)linb::ColT<N>::SMEM);
+    if constexpr (N == 1024)
+      cudaFuncSetAttribute(linb::k2d_colt2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)linb::ColT2<N>::SMEM);
     attrs = true;
   }
   const long long fs2 = (long long)N * N;
@@ -1001,6 +1004,15 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
   auto colpass = [&] {
     if constexpr (N >= 64) {
       if (tma) {
+        if constexpr (N == 1024) {
+          // measured slower (kernel bench 17.08 vs 14.53 ms per 16 config-5-shaped steps): off by default
+          static const bool teams = [] { const char* e = getenv("CHP_COL_TEAMS"); return e && e[0] == '1'; }();
+          if (teams) {
+            linb::k2d_colt2<N><<<dim3(cgrid.x / 2, cgrid.y), linb::ColT2<N>::THREADS, linb::ColT2<N>::SMEM, st>>>(
+                qmap, pmap, ca);
+            return;
+          }
+        }
         linb::k2d_colt<N><<<cgrid, CG::THREADS, linb::ColT<N>::SMEM, st>>>(qmap, pmap, ca);
         return;
       }

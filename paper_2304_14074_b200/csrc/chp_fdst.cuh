@@ -89,11 +89,39 @@ template <int N> struct SmemLd {
   }
 };
 
-// BSYNC: the input is shared by the whole block and reg overlays it (column pass tile):
-// the barrier between the input reads and the first write to reg is a block barrier.
-// OSYNC: out() writes memory that other groups' regions overlay (the column pass's P tile):
-// the barrier between the last read of reg and out() is a block barrier.
-template <int N, bool DS = false, bool PS = false, bool BSYNC = false, bool OSYNC = false, class Ld, class Out>
+// Synchronisation policy of the transform's five phase boundaries.  The phases alternate
+// between shared-memory traffic (L) and FP64 arithmetic (F):
+//   P0 input loads + pre-processing (L) | loaded()      | P1 first DFT + twiddles (F) |
+//   inputs_done() | P2 transpose (L) | transposed() | P3 second DFT (F) | dft2_done() |
+//   P4 Z staging + post-processing + scan (L) | z_read() | P5 out() callbacks (L)
+// WarpSync: the group's data is private, only the warp-level barriers the reuse of reg needs.
+struct WarpSync {
+  CHP_DEV static void loaded() {}
+  CHP_DEV static void inputs_done() { __syncwarp(); }   // input reads done before reg is written
+  CHP_DEV static void transposed() { __syncwarp(); }    // transposed reads done before Z is written
+  CHP_DEV static void dft2_done() {}
+  CHP_DEV static void z_read() { __syncwarp(); }        // Z reads done before out() writes reg
+};
+// BlockIn / BlockOut / BlockInOut: the input is shared by the whole block and reg overlays it
+// (column pass tile) and/or out() writes memory other groups' regions overlay (P tile).
+template <bool IN, bool OUT> struct BlockSync : WarpSync {
+  CHP_DEV static void inputs_done() { if constexpr (IN) __syncthreads(); else __syncwarp(); }
+  CHP_DEV static void z_read() { if constexpr (OUT) __syncthreads(); else __syncwarp(); }
+};
+// PhaseTick: every boundary is a block-wide barrier.  Two teams of warps that run the same
+// transform sequence one phase apart (one team executes one extra barrier first) then always
+// pair one team's L phase with the other's F phase: the shared-memory pipe and the FP64
+// pipes work at the same time instead of in lockstep.
+struct PhaseTick {
+  CHP_DEV static void tick() { asm volatile("bar.sync 0;" ::: "memory"); }
+  CHP_DEV static void loaded() { tick(); }
+  CHP_DEV static void inputs_done() { tick(); }
+  CHP_DEV static void transposed() { tick(); }
+  CHP_DEV static void dft2_done() { tick(); }
+  CHP_DEV static void z_read() { tick(); }
+};
+
+template <int N, bool DS = false, bool PS = false, class Sy = WarpSync, class Ld, class Out>
 CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restrict__ twl, int l,
                       double sa2, double ca2, Out out,
                       const double2* __restrict__ dsc = nullptr,
@@ -128,6 +156,7 @@ CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restr
     z[n2] = make_double2(fma(sp, v.x, smn * w.x), fma(sp, v.y, smn * w.y));
   }
   if (l == 0) z[0] = make_double2(0.0, 0.0);      // x_0 = x_N = 0 (pad slots may hold anything)
+  Sy::loaded();
   wdst::dft<R>(z);
   asm volatile("" : "+l"(twl)::"memory");
 #if CHP_TW_POW
@@ -145,8 +174,7 @@ CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restr
 #pragma unroll
   for (int k2 = 1; k2 < R; ++k2) z[brev(k2, RB)] = wdst::cmul(z[brev(k2, RB)], __ldg(&twl[k2 * L]));
 #endif
-  if constexpr (BSYNC) __syncthreads();            // every group's input reads are done
-  else __syncwarp();                               // every lane's input reads are done
+  Sy::inputs_done();
   double2* tp = reg + l;
 #pragma unroll
   for (int k2 = 0; k2 < R; ++k2) tp[k2 * (L + 1)] = z[brev(k2, RB)];
@@ -158,9 +186,10 @@ CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restr
 #pragma unroll
     for (int n1 = 0; n1 < L; ++n1) v[t][n1] = tr[t * L * (L + 1) + n1];
   }
-  __syncwarp();
+  Sy::transposed();
 #pragma unroll
   for (int t = 0; t < Q; ++t) wdst::dft<L>(v[t]);
+  Sy::dft2_done();
   // Z[k2 + R k1], k2 = l + L t  ->  zaddr = zb + L t + (R + 2) k1 (+ t when Q == 2)
   double2* zw = reg + l + ((Q == 1) ? l / C : 0);
 #pragma unroll
@@ -202,8 +231,7 @@ CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restr
     if (l >= o) { ia += ya; ib += yb; }
   }
   const double offa = ia - sa, offb = ib - sb;
-  if constexpr (OSYNC) __syncthreads();            // every group's Z reads are done
-  else __syncwarp();                               // Z reads done before out() writes reg
+  Sy::z_read();
 #pragma unroll
   for (int j = 0; j < C; ++j) {
     if constexpr (PS)
@@ -221,7 +249,7 @@ CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __r
                       const double2* __restrict__ dsc = nullptr,
                       const double2* __restrict__ dsm = nullptr,
                       const double2* __restrict__ dpo = nullptr) {
-  pair_dst_ld<N, DS, PS, false, false>(SmemLd<N>(src, l), reg, twl, l, sa2, ca2, out, dsc, dsm, dpo);
+  pair_dst_ld<N, DS, PS, WarpSync>(SmemLd<N>(src, l), reg, twl, l, sa2, ca2, out, dsc, dsm, dpo);
 }
 
 // store the transform output into a pair region in p2 layout (k = C l + j):

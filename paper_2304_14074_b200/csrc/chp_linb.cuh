@@ -530,7 +530,7 @@ k2d_colt(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUten
       ob[2 * j + 1] = make_double2(a1, b1);
     };
     // D'' of the column pair scales the forward transform's outputs in its post-processing
-    fdst::pair_dst_ld<N, false, true, true>(TileLd<N>(tile, g, l), reg, twl, l, sa2, ca2, put, nullptr,
+    fdst::pair_dst_ld<N, false, true, fdst::BlockSync<true, false>>(TileLd<N>(tile, g, l), reg, twl, l, sa2, ca2, put, nullptr,
                                             nullptr, dr);
     __syncwarp();
     // P (pair-interleaved): rows (2k, 2k+1), columns (2 kq, 2 kq + 1), k = C l + j
@@ -538,7 +538,7 @@ k2d_colt(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUten
       // tile row j L + l, 16-byte chunks 2g and 2g + 1, XOR-swizzled with the row's low bits
       unsigned char* pt = tile + l * 128;
       const int c0 = ((2 * g) ^ (l & 7)) << 4, c1 = ((2 * g + 1) ^ (l & 7)) << 4;
-      fdst::pair_dst_ld<N, false, false, false, true>(
+      fdst::pair_dst_ld<N, false, false, fdst::BlockSync<false, true>>(
           fdst::SmemLd<N>(reg, l), reg, twl, l, sa2, ca2,
           [&](int j, double a0, double a1, double b0, double b1) {
             *reinterpret_cast<double2*>(pt + j * (L * 128) + c0) = make_double2(a0, a1);
@@ -557,6 +557,80 @@ k2d_colt(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUten
       });
     }
   }
+}
+
+// Two-team column pass (N = 1024): one 256-thread block per SM runs two tiles, one per team
+// of 4 warps, through the same phase sequence ONE PHASE APART (fdst::PhaseTick): while one
+// team's warps move data through shared memory the other team's warps run their DFT on the
+// FP64 pipes.  Warp w of either team sits on scheduler w % 4, so each scheduler always holds
+// one warp of each kind.  Two independent 128-thread blocks per SM (k2d_colt) drift into
+// lockstep instead, where both pipes idle in turn.
+template <int N> struct ColT2 {
+  using CT = ColT<N>;
+  static constexpr int THREADS = 2 * ColG<N>::THREADS;
+  static constexpr size_t TEAM = ((CT::SMEM - 1024) + 1023) / 1024 * 1024;   // per-team bytes
+  static constexpr size_t SMEM = 1024 + 2 * TEAM;
+  static_assert(CT::PSTORE, "two-team column pass: N = 1024 geometry");
+};
+
+template <int N>
+__global__ void __launch_bounds__(ColT2<N>::THREADS, 1)
+k2d_colt2(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap pmap, ColArgs a) {
+  using F = fdst::FG<N>;
+  using CG = ColG<N>;
+  using CT = ColT<N>;
+  using Sy = fdst::PhaseTick;
+  constexpr int L = F::L, TC = CG::TC, TT = CG::THREADS;
+  extern __shared__ __align__(16) unsigned char raw[];
+  __shared__ __align__(8) unsigned long long bar[2];
+  const int team = threadIdx.x / TT, tid = threadIdx.x % TT;
+  unsigned char* tile = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u) + team * ColT2<N>::TEAM;
+  const int g = tid / L, l = tid % L;
+  const int sys = blockIdx.y;
+  const int j0 = (blockIdx.x * 2 + team) * TC;
+  if (tid == 0) {
+    mbar_init(&bar[team], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_proxy();
+    mbar_expect_tx(&bar[team], (unsigned)CT::TILE);
+#pragma unroll
+    for (int b = 0; b < CT::NBOX; ++b)
+      tma_load_2d(tile + (size_t)b * CT::BR * CT::IB, &qmap, j0, sys * N + b * CT::BR, &bar[team]);
+  }
+  const double2 ac = __ldg(&a.wtab[l]);
+  const double sa2 = 2.0 * ac.y, ca2 = 2.0 * ac.x;
+  const double2* twl = a.wtab + N + l;
+  const int kq = qpos_inv<N>(j0 / 2 + g);
+  const double2* dr = a.dtab + (long long)kq * N + l;
+  double2* reg = reinterpret_cast<double2*>(tile) + CG::RBASE(g);
+  __syncthreads();                                       // both barriers are initialised
+  if (team == 1) Sy::tick();                             // team 1 runs one phase behind team 0
+  mbar_wait(&bar[team], 0);
+  {
+    double2* ob = fdst::out_base<N>(reg, l);
+    auto put = [&](int j, double a0, double a1, double b0, double b1) {
+      ob[2 * j] = make_double2(a0, b0);
+      ob[2 * j + 1] = make_double2(a1, b1);
+    };
+    fdst::pair_dst_ld<N, false, true, Sy>(TileLd<N>(tile, g, l), reg, twl, l, sa2, ca2, put, nullptr,
+                                          nullptr, dr);
+    __syncwarp();
+    unsigned char* pt = tile + l * 128;
+    const int c0 = ((2 * g) ^ (l & 7)) << 4, c1 = ((2 * g + 1) ^ (l & 7)) << 4;
+    fdst::pair_dst_ld<N, false, false, Sy>(
+        fdst::SmemLd<N>(reg, l), reg, twl, l, sa2, ca2,
+        [&](int j, double a0, double a1, double b0, double b1) {
+          *reinterpret_cast<double2*>(pt + j * (L * 128) + c0) = make_double2(a0, a1);
+          *reinterpret_cast<double2*>(pt + j * (L * 128) + c1) = make_double2(b0, b1);
+        });
+    fence_async_proxy();
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(TT) : "memory");   // the team's P tile is staged
+    if (tid == 0) {
+      tma_store_3d(&pmap, tile, 4 * qpos_inv<N>(j0 / 2), sys * L, 0);
+      tma_store_commit_wait_read();
+    }
+  }
+  if (team == 0) Sy::tick();                             // matches team 1's leading barrier
 }
 
 }  // namespace linb
