@@ -11,9 +11,14 @@
 // scalars stay on the device (CgSys) and every dot product is a fixed-order
 // two-level reduction.
 //
-// Phases per CG iteration: R1 rows (P update fused, Y = T'_j P), C cols
-// (Y = T'_i (c'' .* T'_i Y)), R3 rows (Y = d .* P + T'_j Y, partial P.Y),
-// reduce (alpha), U (X += alpha P, R -= alpha Y, partials), reduce (beta).
+// Phases per CG iteration: E3 (P = M^-1 R + beta P, streaming), T rows (Y = T'_j P),
+// C cols (Y = T'_i (c'' .* T'_i Y)), T rows (Y = T'_j Y), E1 (Y = d .* P + Y, partial
+// P.Y, streaming), reduce (alpha), E2 (X += alpha P, R -= alpha Y, partials), reduce (beta).
+// The elementwise work runs in streaming kernels (5-6 TB/s) instead of inside the row
+// transforms: fused into the transform kernels (round 1) the same loads sat on the critical
+// path of a one-transform-per-group block at 8 warps/SM -- 556 + 362 us per iteration for the
+// two fused row phases against 2 x (112 + 140) us unfused, although the unfused form moves
+// P and Y once more (profiles/r02_c4_launches_v0.txt, all 128 config-4 systems active).
 
 struct Pcg2 {
   int m;
@@ -105,17 +110,15 @@ __global__ void k_pcg2_prep(Pcg2 a) {
   }
 }
 
-// rows: op 0: out = T' in ; op 1: P update + Y = T' P ; op 2: out = Dk .* P + T' in (+ partial)
-template <int N, int OP>
+// rows: out = T'_j in (PI -> PI)
+template <int N>
 __global__ void __launch_bounds__(128, 2) k_pcg2_rows(Pcg2 a, const double* in, double* out, int loop) {
   using F = fdst::FG<N>;
   using G2 = Pcg2G<N>;
   constexpr int L = F::L, R = F::R, Q = F::Q;
   extern __shared__ __align__(16) double2 smp[];
-  __shared__ double wpart[G2::GPB];
   const int sys = blockIdx.y;
-  const CgSys& q = a.cg[sys];
-  if (pcg2_skip(q, loop)) return;
+  if (pcg2_skip(a.cg[sys], loop)) return;
   const long long NN = (long long)N * N;
   const int g = threadIdx.x / L, l = threadIdx.x % L;
   const int s = blockIdx.x * G2::GPB + g;
@@ -124,31 +127,10 @@ __global__ void __launch_bounds__(128, 2) k_pcg2_rows(Pcg2 a, const double* in, 
   double2* reg = smp + G2::RBASE(g);
   const double2 ac = __ldg(&a.wtab[l]);
   const double2* twl = a.wtab + N + l;
-  if (OP == 1) {
-    const double2* Rr = reinterpret_cast<const double2*>(a.R) + base;
-    const double2* Dr = reinterpret_cast<const double2*>(a.Dk) + (long long)(have ? s : 0) * N;
-    double2* Pr = reinterpret_cast<double2*>(a.P) + base;
-    const bool first = q.iters == 0;
-    const double beta = q.beta, acb = q.acbar;
+  const double2* src = reinterpret_cast<const double2*>(in) + base;
 #pragma unroll 8
-    for (int i = 0; i < R; ++i) {
-      const int n = l + L * i;
-      const double2 r = Rr[n], mi = pcg2_mi(Dr[n], acb);
-      double2 p;
-      if (first) p = make_double2(r.x * mi.x, r.y * mi.y);
-      else {
-        const double2 po = Pr[n];
-        p = make_double2(fma(beta, po.x, r.x * mi.x), fma(beta, po.y, r.y * mi.y));
-      }
-      if (have) Pr[n] = p;
-      reg[n + i / Q] = p;
-    }
-  } else {
-    const double2* src = reinterpret_cast<const double2*>(in) + base;
-#pragma unroll 8
-    for (int i = 0; i < R; ++i) linb::cp16(&reg[l + L * i + i / Q], &src[l + L * i]);
-    linb::cp_wait();
-  }
+  for (int i = 0; i < R; ++i) linb::cp16(&reg[l + L * i + i / Q], &src[l + L * i]);
+  linb::cp_wait();
   __syncwarp();
   double2* ob = fdst::out_base<N>(reg, l);
   fdst::pair_dst<N>(reg, reg, twl, l, 2.0 * ac.y, 2.0 * ac.x,
@@ -157,32 +139,8 @@ __global__ void __launch_bounds__(128, 2) k_pcg2_rows(Pcg2 a, const double* in, 
                       ob[2 * j + 1] = make_double2(a1, b1);
                     });
   __syncwarp();
-  double2* dst = reinterpret_cast<double2*>(out) + base;
-  if (OP == 2) {
-    const double2* Pr = reinterpret_cast<const double2*>(a.P) + base;
-    const double2* Dr = reinterpret_cast<const double2*>(a.Dk) + (long long)(have ? s : 0) * N;
-    double part = 0.0;
-#pragma unroll 8
-    for (int i = 0; i < R; ++i) {
-      const int n = l + L * i;
-      const double2 y = reg[n + i / Q], p = Pr[n], d = Dr[n];
-      const double2 o = make_double2(fma(d.x, p.x, y.x), fma(d.y, p.y, y.y));
-      if (have) {
-        dst[n] = o;
-        part = fma(p.x, o.x, part);
-        part = fma(p.y, o.y, part);
-      }
-    }
-    // fixed-order block partial: lanes of the group, then groups in order
-    for (int o = L / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o, L);
-    if (l == 0) wpart[g] = part;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int k = 0; k < G2::GPB; ++k) t += wpart[k];
-      a.partial[(long long)sys * G2::RBLK + blockIdx.x] = t;
-    }
-  } else if (have) {
+  if (have) {
+    double2* dst = reinterpret_cast<double2*>(out) + base;
 #pragma unroll 8
     for (int i = 0; i < R; ++i) dst[l + L * i] = reg[l + L * i + i / Q];
   }
@@ -291,6 +249,62 @@ __global__ void k_pcg2_init(Pcg2 a) {
     v2 = fma(r.y, r.y, v2);
   }
   pcg2_block_pair(v1, v2, a.partial + ((long long)s * kPB + blockIdx.x) * 2);
+}
+
+// E3: P = Mi .* R (+ beta P after the first iteration)
+template <int N>
+__global__ void k_pcg2_pdir(Pcg2 a) {
+  const int s = blockIdx.y;
+  const CgSys& q = a.cg[s];
+  if (pcg2_skip(q, true)) return;
+  const long long NN = (long long)N * N, o = (long long)s * (NN / 2);
+  const double2* R = reinterpret_cast<const double2*>(a.R) + o;
+  double2* P = reinterpret_cast<double2*>(a.P) + o;
+  const double2* Dk = reinterpret_cast<const double2*>(a.Dk);
+  const bool first = q.iters == 0;
+  const double beta = q.beta, acb = q.acbar;
+#pragma unroll 4
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < NN / 2;
+       t += (long long)gridDim.x * blockDim.x) {
+    const double2 r = R[t], mi = pcg2_mi(Dk[t], acb);
+    double2 p = make_double2(r.x * mi.x, r.y * mi.y);
+    if (!first) {
+      const double2 po = P[t];
+      p = make_double2(fma(beta, po.x, p.x), fma(beta, po.y, p.y));
+    }
+    P[t] = p;
+  }
+}
+
+// E1: Y = Dk .* P + Y (Y = a S (c .* S P) on entry: Y = A P) ; partial P.Y
+template <int N>
+__global__ void k_pcg2_aptail(Pcg2 a, int loop) {
+  const int s = blockIdx.y;
+  if (pcg2_skip(a.cg[s], loop)) return;
+  const long long NN = (long long)N * N, o = (long long)s * (NN / 2);
+  const double2* P = reinterpret_cast<const double2*>(a.P) + o;
+  double2* Y = reinterpret_cast<double2*>(a.Y) + o;
+  const double2* Dk = reinterpret_cast<const double2*>(a.Dk);
+  double v1 = 0.0;
+#pragma unroll 4
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < NN / 2;
+       t += (long long)gridDim.x * blockDim.x) {
+    const double2 p = P[t], d = Dk[t], y = Y[t];
+    const double2 w = make_double2(fma(d.x, p.x, y.x), fma(d.y, p.y, y.y));
+    Y[t] = w;
+    v1 = fma(p.x, w.x, v1);
+    v1 = fma(p.y, w.y, v1);
+  }
+  // fixed-order block partial (single value per block, kPB blocks per system)
+  __shared__ double w1[32];
+  for (int of = 16; of > 0; of >>= 1) v1 += __shfl_xor_sync(0xffffffffu, v1, of);
+  if ((threadIdx.x & 31) == 0) w1[threadIdx.x >> 5] = v1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t1 = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t1 += w1[k];
+    a.partial[(long long)s * kPB + blockIdx.x] = t1;
+  }
 }
 
 // X += alpha P ; R -= alpha Y ; partials (R.Mi R, R.R)
