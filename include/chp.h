@@ -152,6 +152,58 @@ chp_status chp_coarse_sweep(chp_ctx* ctx, const chp_grid* g, const chp_spec* coa
                             unsigned char* changed, double* inc,
                             chp_sys_info* info, void* stream);
 
+/*
+ * Device-initiated boundary hand-off of the sharded coarse chain (SURVEY.md 8(e),
+ * 8(f2); replaces the per-hop dist.send/recv of the slice end state around the
+ * sequential sweep of parareal.py:245-251).  The sending rank's sweep stores
+ * U[n_end] of every IC, and its "changed in this sweep" flags, straight into a
+ * mailbox in the receiving rank's memory (a peer mapping: cudaIpc between
+ * processes, or plain device memory for shards on one device) and then releases
+ * *peer_flag = seq (system scope).  In the 2D LINEAR_A cooperative kernel the stores
+ * are fused into the last slice's correction; other coarse paths run a put kernel
+ * after the sweep.  The receiver's stream waits on its flag (chp_hop_wait: a
+ * stream memory operation, no kernel spins), takes the mailbox (chp_hop_take) and
+ * acknowledges by releasing `seq` into the sender's ack word.
+ */
+typedef struct {
+  double* peer_u;               /* IC i's field goes to peer_u + i * peer_stride */
+  long long peer_stride;
+  unsigned char* peer_changed;  /* nic bytes: bit 0 of changed[i][n_end] */
+  unsigned int* peer_flag;      /* released with seq after the data */
+  unsigned int seq;
+  unsigned int pad_;
+} chp_hop;
+
+/* chp_coarse_sweep followed by (or fused with) the hand-off described by `hop`
+ * (hop == NULL: exactly chp_coarse_sweep). */
+chp_status chp_coarse_sweep_hop(chp_ctx* ctx, const chp_grid* g, const chp_spec* coarse,
+                                int mode, int nic, int nslices, int n_begin, int n_end,
+                                double* U, const double* F, double* G,
+                                long long ic_stride, long long slice_stride,
+                                unsigned char* changed, double* inc,
+                                chp_sys_info* info, const chp_hop* hop, void* stream);
+
+/* Work queued on `stream` after this call starts once *flag >= seq (flag: device
+ * memory of this context's device; cuStreamWaitValue32, no kernel). */
+chp_status chp_hop_wait(chp_ctx* ctx, const unsigned int* flag, unsigned int seq, void* stream);
+
+/* Take a received boundary: for every IC whose freeze bit (bit 1 of changed[i *
+ * changed_stride]) is clear, U0[i * ic_stride] = mail[i * mail_stride] and bit 0 of
+ * changed[i * changed_stride] = bit 0 of mail_changed[i]; then release *peer_ack =
+ * seq (peer_ack may be NULL). */
+chp_status chp_hop_take(chp_ctx* ctx, const chp_grid* g, int nic, const double* mail,
+                        long long mail_stride, const unsigned char* mail_changed, double* U0,
+                        long long ic_stride, unsigned char* changed, long long changed_stride,
+                        unsigned int* peer_ack, unsigned int seq, void* stream);
+
+/* Mailbox memory: plain cudaMalloc allocations (zero-filled) that can be shared with
+ * another process on the node.  handle: 64 bytes (cudaIpcMemHandle_t). */
+chp_status chp_mem_alloc(chp_ctx* ctx, long long bytes, void** dptr);
+chp_status chp_mem_free(chp_ctx* ctx, void* dptr);
+chp_status chp_ipc_export(chp_ctx* ctx, void* dptr, unsigned char* handle64);
+chp_status chp_ipc_open(chp_ctx* ctx, const unsigned char* handle64, void** dptr);
+chp_status chp_ipc_close(chp_ctx* ctx, void* dptr);
+
 /* max |a - b| over n_fields fields of `size` entries (row pitch aware),
  * max-accumulated into out[0] (device). */
 chp_status chp_max_abs_diff(chp_ctx* ctx, const chp_grid* g, int n_fields,

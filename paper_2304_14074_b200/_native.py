@@ -25,6 +25,8 @@ EXPORTS = (
     "chp_version", "chp_status_str", "chp_ctx_create", "chp_ctx_destroy", "chp_last_error",
     "chp_sysinfo_reset", "chp_propagate", "chp_coarse_sweep", "chp_max_abs_diff",
     "chp_debug_trace", "chp_nn_propagate", "chp_propagate_hist", "chp_field_stats", "chp_probe_dfma",
+    "chp_coarse_sweep_hop", "chp_hop_wait", "chp_hop_take", "chp_mem_alloc", "chp_mem_free",
+    "chp_ipc_export", "chp_ipc_open", "chp_ipc_close",
 )
 
 
@@ -45,6 +47,13 @@ class ChpNNParams(C.Structure):
     _fields_ = [("n_subdomains", C.c_int), ("max_iter", C.c_int), ("warm_start", C.c_int),
                 ("pad_", C.c_int), ("theta", C.c_double), ("tol", C.c_double),
                 ("h2", C.c_double)]
+
+
+class ChpHop(C.Structure):
+    """include/chp.h chp_hop: the fused boundary hand-off of the sharded coarse chain."""
+    _fields_ = [("peer_u", C.c_void_p), ("peer_stride", C.c_longlong),
+                ("peer_changed", C.c_void_p), ("peer_flag", C.c_void_p),
+                ("seq", C.c_uint), ("pad_", C.c_uint)]
 
 
 class ChpSysInfo(C.Structure):
@@ -85,6 +94,15 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                 ll, vp, vp, vp]
     L.chp_coarse_sweep.argtypes = [vp, C.POINTER(ChpGrid), C.POINTER(ChpSpec), i, i, i, i, i,
                                    vp, vp, vp, ll, ll, vp, vp, vp, vp]
+    L.chp_coarse_sweep_hop.argtypes = [vp, C.POINTER(ChpGrid), C.POINTER(ChpSpec), i, i, i, i, i,
+                                       vp, vp, vp, ll, ll, vp, vp, vp, C.POINTER(ChpHop), vp]
+    L.chp_hop_wait.argtypes = [vp, vp, C.c_uint, vp]
+    L.chp_hop_take.argtypes = [vp, C.POINTER(ChpGrid), i, vp, ll, vp, vp, ll, vp, ll, vp, C.c_uint, vp]
+    L.chp_mem_alloc.argtypes = [vp, ll, C.POINTER(vp)]
+    L.chp_mem_free.argtypes = [vp, vp]
+    L.chp_ipc_export.argtypes = [vp, vp, C.c_char_p]
+    L.chp_ipc_open.argtypes = [vp, C.c_char_p, C.POINTER(vp)]
+    L.chp_ipc_close.argtypes = [vp, vp]
     L.chp_max_abs_diff.argtypes = [vp, C.POINTER(ChpGrid), i, vp, ll, vp, ll, vp, vp]
     L.chp_debug_trace.argtypes = [vp, i]
     L.chp_field_stats.argtypes = [vp, C.POINTER(ChpGrid), i, vp, ll, vp, vp]

@@ -1058,7 +1058,7 @@ template <int N>
 cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, int nic, int nsl,
                     int n0, int n1, double* U, const double* F, double* G, long long ics,
                     long long sls, unsigned char* changed, double* inc, chp_sys_info* info,
-                    const NTables& nt, cudaStream_t st) {
+                    const NTables& nt, cudaStream_t st, const chp_hop* hop, bool* fused) {
   const long long fs = (long long)g.m * N;
   // LINEAR_A coarse: the whole sweep in one cooperative persistent kernel
   // (chp_coarse2.cuh, no host round trips); other coarse schemes: one batched
@@ -1105,6 +1105,11 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
     }
     cudaMemsetAsync(ca.bar, 0, sizeof(unsigned int), st);
     ca.lam = nt.lam; ca.wtab = nt.wtab;
+    if (hop) {
+      ca.hop_u = hop->peer_u; ca.hop_stride = hop->peer_stride; ca.hop_changed = hop->peer_changed;
+      ca.hop_flag = hop->peer_flag; ca.hop_seq = hop->seq;
+      *fused = true;
+    }
     void* args[] = {&ca};
     return cudaLaunchCooperativeKernel((void*)k2d_coarse2<N>, dim3(blocks), dim3(G2::THREADS),
                                        args, G2::SMEM, st);
@@ -1190,7 +1195,9 @@ cudaError_t chp2d_coarse_sweep(Chp2d* c, const chp_grid& g, const chp_spec& sp, 
                                int nic, int nsl, int n0, int n1, double* U, const double* F,
                                double* G, long long ic_stride, long long sl_stride,
                                unsigned char* changed, double* inc, chp_sys_info* info,
-                               cudaStream_t st, std::string* err) {
+                               cudaStream_t st, std::string* err, const chp_hop* hop,
+                               bool* fused) {
+  *fused = false;
   if (!pow2_ok(g, err)) return cudaSuccess;
   const int N = g.m + 1;
   const NTables* nt = nullptr;
@@ -1199,7 +1206,7 @@ cudaError_t chp2d_coarse_sweep(Chp2d* c, const chp_grid& g, const chp_spec& sp, 
   c->hist = nullptr;            // coarse steps never record a residual history
   c->hlen = 0;
   CHP_N_SWITCH(N, return sweep_n<NN>(c, g, sp, mode, nic, nsl, n0, n1, U, F, G, ic_stride,
-                                     sl_stride, changed, inc, info, *nt, st));
+                                     sl_stride, changed, inc, info, *nt, st, hop, fused));
   *err = "unsupported N";
   return cudaSuccess;
 }

@@ -1,3 +1,5 @@
+#include <cuda.h>
+#include <string.h>
 // C ABI of libchp.so (include/chp.h): context, caches, dispatch.
 #include <stdio.h>
 #include <string.h>
@@ -45,7 +47,14 @@ cudaError_t chp2d_coarse_sweep(Chp2d* c, const chp_grid& g, const chp_spec& sp, 
                                int nic, int nsl, int n0, int n1, double* U, const double* F,
                                double* G, long long ic_stride, long long sl_stride,
                                unsigned char* changed, double* inc, chp_sys_info* info,
-                               cudaStream_t st, std::string* err);
+                               cudaStream_t st, std::string* err, const chp_hop* hop, bool* fused);
+cudaError_t chp_launch_hop_put(long long fs, int nic, const double* src, long long src_stride,
+                               const unsigned char* changed, long long changed_stride,
+                               const chp_hop& hop, cudaStream_t st);
+cudaError_t chp_launch_hop_take(long long fs, int nic, const double* mail, long long mail_stride,
+                                const unsigned char* mail_changed, double* U0, long long ic_stride,
+                                unsigned char* changed, long long changed_stride,
+                                unsigned int* peer_ack, unsigned int seq, cudaStream_t st);
 
 struct chp_ctx {
   int device = 0;
@@ -264,6 +273,14 @@ chp_status chp_coarse_sweep(chp_ctx* c, const chp_grid* g, const chp_spec* sp, i
                             int nsl, int n0, int n1, double* U, const double* F, double* G,
                             long long ic_stride, long long sl_stride, unsigned char* changed,
                             double* inc, chp_sys_info* info, void* stream) {
+  return chp_coarse_sweep_hop(c, g, sp, mode, nic, nsl, n0, n1, U, F, G, ic_stride, sl_stride,
+                              changed, inc, info, nullptr, stream);
+}
+
+chp_status chp_coarse_sweep_hop(chp_ctx* c, const chp_grid* g, const chp_spec* sp, int mode, int nic,
+                                int nsl, int n0, int n1, double* U, const double* F, double* G,
+                                long long ic_stride, long long sl_stride, unsigned char* changed,
+                                double* inc, chp_sys_info* info, const chp_hop* hop, void* stream) {
   if (!c) return CHP_ERR_ARG;
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard dg(c->device);
@@ -274,8 +291,17 @@ chp_status chp_coarse_sweep(chp_ctx* c, const chp_grid* g, const chp_spec* sp, i
     return fail(c, CHP_ERR_ARG, "bad slice range");
   if (!U || !G || !info || (mode == 1 && (!F || !changed)))
     return fail(c, CHP_ERR_ARG, "bad arrays");
-  if (n0 == n1) return CHP_OK;
+  if (hop && (!hop->peer_u || !hop->peer_flag || (mode == 1 && !hop->peer_changed)))
+    return fail(c, CHP_ERR_ARG, "bad hop descriptor");
   cudaStream_t st = (cudaStream_t)stream;
+  const long long fsz = g->dim == 1 ? (long long)g->m : (long long)g->m * g->pitch;
+  // the hand-off after (not fused into) the sweep: U[n1] and changed[n1] of every IC
+  auto put = [&]() -> chp_status {
+    cudaError_t pe = chp_launch_hop_put(fsz, nic, U + (long long)n1 * sl_stride, ic_stride,
+                                        mode == 1 ? changed + n1 : nullptr, nsl + 1, *hop, st);
+    return pe == cudaSuccess ? CHP_OK : cuda_fail(c, pe, "chp_hop_put");
+  };
+  if (n0 == n1) return hop ? put() : CHP_OK;
   if (g->dim == 1) {
     const double* fac = nullptr;
     if (sp->scheme == CHP_LINEAR_B) {
@@ -290,12 +316,96 @@ chp_status chp_coarse_sweep(chp_ctx* c, const chp_grid* g, const chp_spec* sp, i
     double* tmp = yh + (size_t)g->m * nic;
     cudaError_t e = chp1d_coarse_sweep(*g, *sp, mode, nic, nsl, n0, n1, U, F, G, ic_stride,
                                        sl_stride, changed, inc, fac, ub, yh, tmp, info, st);
-    return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp1d_coarse_sweep");
+    if (e != cudaSuccess) return cuda_fail(c, e, "chp1d_coarse_sweep");
+    return hop ? put() : CHP_OK;
   }
+  bool fused = false;
   cudaError_t e = chp2d_coarse_sweep(c->d2, *g, *sp, mode, nic, nsl, n0, n1, U, F, G, ic_stride,
-                                     sl_stride, changed, inc, info, st, &why);
+                                     sl_stride, changed, inc, info, st, &why, hop, &fused);
   if (!why.empty()) return fail(c, CHP_ERR_UNSUPPORTED, why);
-  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp2d_coarse_sweep");
+  if (e != cudaSuccess) return cuda_fail(c, e, "chp2d_coarse_sweep");
+  return (hop && !fused) ? put() : CHP_OK;
+}
+
+chp_status chp_hop_wait(chp_ctx* c, const unsigned int* flag, unsigned int seq, void* stream) {
+  if (!c || !flag) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  typedef CUresult (*WaitFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static WaitFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<WaitFn>(f);
+  }();
+  if (!fn) return fail(c, CHP_ERR_UNSUPPORTED, "cuStreamWaitValue32 is not available");
+  const CUresult r = fn((CUstream)stream, (CUdeviceptr)(uintptr_t)flag, seq, CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? CHP_OK : fail(c, CHP_ERR_CUDA, "cuStreamWaitValue32 failed");
+}
+
+chp_status chp_hop_take(chp_ctx* c, const chp_grid* g, int nic, const double* mail,
+                        long long mail_stride, const unsigned char* mail_changed, double* U0,
+                        long long ic_stride, unsigned char* changed, long long changed_stride,
+                        unsigned int* peer_ack, unsigned int seq, void* stream) {
+  if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  std::string why;
+  if (!grid_ok(g, &why)) return fail(c, CHP_ERR_ARG, why);
+  if (nic < 1 || !mail || !mail_changed || !U0 || !changed) return fail(c, CHP_ERR_ARG, "bad arrays");
+  const long long fsz = g->dim == 1 ? (long long)g->m : (long long)g->m * g->pitch;
+  cudaError_t e = chp_launch_hop_take(fsz, nic, mail, mail_stride, mail_changed, U0, ic_stride,
+                                      changed, changed_stride, peer_ack, seq, (cudaStream_t)stream);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp_hop_take");
+}
+
+chp_status chp_mem_alloc(chp_ctx* c, long long bytes, void** dptr) {
+  if (!c || !dptr || bytes <= 0) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  cudaError_t e = cudaMalloc(dptr, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaMemset(*dptr, 0, (size_t)bytes);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp_mem_alloc");
+}
+
+chp_status chp_mem_free(chp_ctx* c, void* dptr) {
+  if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  cudaError_t e = cudaFree(dptr);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "chp_mem_free");
+}
+
+chp_status chp_ipc_export(chp_ctx* c, void* dptr, unsigned char* handle64) {
+  if (!c || !dptr || !handle64) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "handle size");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, dptr);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaIpcGetMemHandle");
+  memcpy(handle64, &h, 64);
+  return CHP_OK;
+}
+
+chp_status chp_ipc_open(chp_ctx* c, const unsigned char* handle64, void** dptr) {
+  if (!c || !dptr || !handle64) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "cudaIpcOpenMemHandle");
+}
+
+chp_status chp_ipc_close(chp_ctx* c, void* dptr) {
+  if (!c) return CHP_ERR_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  cudaError_t e = cudaIpcCloseMemHandle(dptr);
+  return e == cudaSuccess ? CHP_OK : cuda_fail(c, e, "cudaIpcCloseMemHandle");
 }
 
 chp_status chp_max_abs_diff(chp_ctx* c, const chp_grid* g, int n_fields, const double* a,

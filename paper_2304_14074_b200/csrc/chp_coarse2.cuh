@@ -48,6 +48,10 @@ struct Coop2Args {
   const double* lam; const double2* wtab;
   unsigned long long* trace;
   int trace_cap, pad2_;
+  // fused boundary hand-off (include/chp.h chp_hop): U[n1] of every IC is also stored to
+  // the next rank's mailbox by the last slice's correction, then the flag is released
+  double* hop_u; long long hop_stride;
+  unsigned char* hop_changed; unsigned int* hop_flag; unsigned int hop_seq, pad3_;
 };
 
 template <int N> struct Coop2G {
@@ -368,12 +372,14 @@ __global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
       const double* gsrc = solve ? a.gx : gn;
       const long long tot = (long long)m * N;
       bool any = false, bad = false;
+      double* hop = (a.hop_u && n == a.n1 - 1) ? a.hop_u + ic * a.hop_stride : nullptr;
       for (long long t = gtid; t < tot; t += gstride) {
         const int j = (int)(t % N);
         const double gv = (j > 0) ? gsrc[t] : 0.0;
         if (a.mode == 0) {
           un1[t] = gv;
           gn[t] = gv;
+          if (hop) hop[t] = gv;
           bad |= !isfinite(gv);
           continue;
         }
@@ -384,7 +390,9 @@ __global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
         bad |= !isfinite(nv) || !isfinite(gv);
         un1[t] = nv;
         gn[t] = gv;
+        if (hop) hop[t] = nv;
       }
+      if (hop) __threadfence_system();
       if (a.mode == 1) {
         if (__syncthreads_or(any) && threadIdx.x == 0) ch[n + 1] = 1;
       }
@@ -395,6 +403,16 @@ __global__ void __launch_bounds__(128, 2) k2d_coarse2(Coop2Args a) {
       for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
       if ((threadIdx.x & 31) == 0) atomic_max_nonneg(a.inc + ic, dmax);
     }
-    gbar(grid);
+        gbar(grid);
+  }
+  // every block's mailbox stores are fenced and ordered before the last barrier: one
+  // thread forwards the changed bits and releases the flag (frozen ICs were skipped: the
+  // receiver keeps its own boundary for those)
+  if (a.hop_flag && gtid == 0) {
+    if (a.hop_changed && a.changed)
+      for (int ic = 0; ic < a.nic; ++ic)
+        a.hop_changed[ic] = a.changed[(long long)ic * (a.nsl + 1) + a.n1] & 1;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.hop_flag), "r"(a.hop_seq) : "memory");
   }
 }

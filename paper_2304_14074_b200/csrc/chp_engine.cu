@@ -124,3 +124,68 @@ cudaError_t chp_launch_dfma_probe(int blocks, int iters, double* out, cudaStream
   k_dfma_probe<<<blocks, 256, 0, st>>>(iters, out);
   return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// Boundary hand-off of the sharded coarse chain (include/chp.h chp_hop).
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void k_hop_put(long long fs, int nic, const double* __restrict__ src, long long src_stride,
+                          double* __restrict__ dst, long long dst_stride) {
+  const long long total = fs * nic;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / fs, o = t % fs;
+    dst[i * dst_stride + o] = src[i * src_stride + o];
+  }
+  __threadfence_system();
+}
+
+// one thread: the changed bytes, then the flag (release, system scope)
+__global__ void k_hop_signal(int nic, const unsigned char* changed, long long changed_stride,
+                             unsigned char* peer_changed, unsigned int* flag, unsigned int seq) {
+  if (changed && peer_changed)
+    for (int i = 0; i < nic; ++i) peer_changed[i] = changed[i * changed_stride] & 1;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
+}
+
+__global__ void k_hop_take(long long fs, int nic, const double* __restrict__ mail, long long mail_stride,
+                           const unsigned char* mail_changed, double* __restrict__ U0,
+                           long long ic_stride, unsigned char* changed, long long changed_stride) {
+  const long long total = fs * nic;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / fs, o = t % fs;
+    const unsigned char c = changed[i * changed_stride];
+    if (c & 2) continue;                                   // frozen IC: keeps its boundary
+    U0[i * ic_stride + o] = mail[i * mail_stride + o];
+    if (o == 0) changed[i * changed_stride] = (unsigned char)((c & 2) | (mail_changed[i] & 1));
+  }
+}
+
+}  // namespace
+
+cudaError_t chp_launch_hop_put(long long fs, int nic, const double* src, long long src_stride,
+                               const unsigned char* changed, long long changed_stride,
+                               const chp_hop& hop, cudaStream_t st) {
+  if (src) {
+    long long blocks = (fs * nic + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_hop_put<<<(int)blocks, 256, 0, st>>>(fs, nic, src, src_stride, hop.peer_u, hop.peer_stride);
+  }
+  k_hop_signal<<<1, 1, 0, st>>>(nic, changed, changed_stride, hop.peer_changed, hop.peer_flag, hop.seq);
+  return cudaGetLastError();
+}
+
+cudaError_t chp_launch_hop_take(long long fs, int nic, const double* mail, long long mail_stride,
+                                const unsigned char* mail_changed, double* U0, long long ic_stride,
+                                unsigned char* changed, long long changed_stride,
+                                unsigned int* peer_ack, unsigned int seq, cudaStream_t st) {
+  long long blocks = (fs * nic + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_hop_take<<<(int)blocks, 256, 0, st>>>(fs, nic, mail, mail_stride, mail_changed, U0, ic_stride,
+                                         changed, changed_stride);
+  if (peer_ack) k_hop_signal<<<1, 1, 0, st>>>(0, nullptr, 0, nullptr, peer_ack, seq);
+  return cudaGetLastError();
+}

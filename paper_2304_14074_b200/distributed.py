@@ -83,6 +83,120 @@ class _LoopbackEnd:
         return None                      # SimulatedRanks reduces across shards itself
 
 
+class Mailbox:
+    """One rank's receive side of the device-initiated hop (include/chp.h chp_hop): two
+    slots of [B] boundary fields + [B] changed bytes, the flag the sender releases and the
+    ack word this rank's *own* sends wait on, in one chp_mem_alloc allocation (so it can
+    be exported with cudaIpc).  Layout (bytes): slot s field i at s*B*fs*8 + i*fs*8;
+    changed at 2*B*fs*8 + s*B; flag at 2*B*fs*8 + 64 + ... (256-byte aligned words)."""
+
+    def __init__(self, ctx, B: int, fs: int):
+        import ctypes
+        self.ctx, self.B, self.fs = ctx, B, fs
+        self.off_changed = 2 * B * fs * 8
+        self.off_flag = (self.off_changed + 2 * B + 255) // 256 * 256
+        self.off_ack = self.off_flag + 256
+        self.bytes = self.off_ack + 256
+        p = ctypes.c_void_p()
+        ctx.check(ctx.L.chp_mem_alloc(ctx.h, self.bytes, ctypes.byref(p)), "chp_mem_alloc")
+        self.base = p.value
+
+    def handle(self) -> bytes:
+        import ctypes
+        buf = ctypes.create_string_buffer(64)
+        self.ctx.check(self.ctx.L.chp_ipc_export(self.ctx.h, ctypes.c_void_p(self.base), buf),
+                       "chp_ipc_export")
+        return buf.raw
+
+    def free(self):
+        import ctypes
+        if self.base:
+            self.ctx.L.chp_mem_free(self.ctx.h, ctypes.c_void_p(self.base))
+            self.base = 0
+
+
+class HopComm:
+    """Device-initiated coarse-chain hand-off instead of dist.send/recv:
+    rank r's coarse sweep stores U_{s1} straight into rank r+1's mailbox and releases a
+    flag (fused into the cooperative 2D kernel's last correction; a put kernel otherwise);
+    rank r+1's stream waits on the flag with a stream memory operation (no kernel spins),
+    takes the mailbox and acknowledges into rank r's ack word, which gates the reuse of
+    the mailbox slot two sends later.  ``peers``: {rank: base address of that rank's
+    mailbox as seen from this process} -- cudaIpc mappings between processes
+    (``HopComm.over_ipc``), or the plain addresses of shards living in one process
+    (``HopComm.loopback``, the simulated ranks of tests/test_gpu_sharded.py).  The
+    increment all-reduce stays on torch.distributed (``red``)."""
+
+    fused = True
+
+    def __init__(self, rank: int, world: int, box: Mailbox, peers: dict, red=None):
+        self.rank, self.world, self.box, self.peers, self.red = rank, world, box, peers, red
+        self.seq_out = 0
+        self.seq_in = 0
+
+    # -- construction ----------------------------------------------------------
+    @classmethod
+    def loopback(cls, ctx, world: int, B: int, fs: int):
+        boxes = [Mailbox(ctx, B, fs) for _ in range(world)]
+        peers = {r: boxes[r].base for r in range(world)}
+        return [cls(r, world, boxes[r], peers) for r in range(world)]
+
+    @classmethod
+    def over_ipc(cls, ctx, rank: int, world: int, B: int, fs: int):
+        """Exchange the mailboxes' cudaIpc handles over torch.distributed and map the
+        neighbours' (one process per GPU on one node)."""
+        import ctypes
+
+        import torch.distributed as dist
+        box = Mailbox(ctx, B, fs)
+        handles = [None] * world
+        dist.all_gather_object(handles, box.handle())
+        peers = {rank: box.base}
+        for r in (rank - 1, rank + 1):
+            if 0 <= r < world:
+                p = ctypes.c_void_p()
+                ctx.check(ctx.L.chp_ipc_open(ctx.h, handles[r], ctypes.byref(p)), "chp_ipc_open")
+                peers[r] = p.value
+        return cls(rank, world, box, peers, red=TorchComm(rank, world))
+
+    # -- the hop -----------------------------------------------------------------
+    def hop(self, stream_ptr):
+        """Descriptor of the next send (to rank+1), after gating on the slot's ack."""
+        import ctypes
+
+        from . import _native as N
+        self.seq_out += 1
+        seq, b = self.seq_out, self.box
+        if seq > 2:        # slot seq % 2 last carried message seq - 2: wait until it was taken
+            b.ctx.check(b.ctx.L.chp_hop_wait(b.ctx.h, ctypes.c_void_p(b.base + b.off_ack), seq - 2,
+                                             stream_ptr), "chp_hop_wait")
+        dst = self.peers[self.rank + 1]
+        slot = seq % 2
+        return N.ChpHop(dst + slot * b.B * b.fs * 8, b.fs, dst + b.off_changed + slot * b.B,
+                        dst + b.off_flag, seq, 0)
+
+    def take(self, eng, grid_native, stream_ptr) -> None:
+        """Wait for the next message from rank-1 and move it into local slot 0."""
+        import ctypes
+
+        from . import _native as N
+        self.seq_in += 1
+        seq, b = self.seq_in, self.box
+        L = b.ctx.L
+        b.ctx.check(L.chp_hop_wait(b.ctx.h, ctypes.c_void_p(b.base + b.off_flag), seq, stream_ptr),
+                    "chp_hop_wait")
+        slot = seq % 2
+        ack = self.peers[self.rank - 1] + b.off_ack
+        b.ctx.check(L.chp_hop_take(
+            b.ctx.h, grid_native, b.B, ctypes.c_void_p(b.base + slot * b.B * b.fs * 8), b.fs,
+            ctypes.c_void_p(b.base + b.off_changed + slot * b.B), N.ptr(eng.U),
+            eng.U.shape[1] * eng.U.shape[2], N.ptr(eng.changed), eng.changed.shape[1],
+            ctypes.c_void_p(ack), seq, stream_ptr), "chp_hop_take")
+
+    def all_reduce_max(self, t, async_op: bool = False):
+        return None if self.red is None else self.red.all_reduce_max(t, async_op=async_op)
+
+
 class ShardedParareal:
     """Parareal on one rank's contiguous slice shard, for ``batch`` independent ICs
     (all ICs of those slices live on the rank)."""
@@ -124,6 +238,10 @@ class ShardedParareal:
         local freeze bit (bit 1 of slot 0) is kept."""
         if self.rank == 0:
             return
+        if getattr(self.comm, "fused", False):
+            from . import _native as N
+            self.comm.take(self.eng, self.eng._native_grid(), N.stream_ptr(None, self.eng.device))
+            return
         torch = self._torch
         dev = self.eng.U.device
         buf = torch.empty((self.B, self.eng.U.shape[2]), dtype=torch.float64, device=dev)
@@ -133,8 +251,15 @@ class ShardedParareal:
         self.comm.recv(flag, src=self.rank - 1)
         self.eng.changed[:, 0] = (self.eng.changed[:, 0] & 2) | (flag & 1)
 
+    def _hop(self):
+        """The fused hand-off descriptor of this sweep (None: last rank, or send/recv comm)."""
+        if self.rank == self.world - 1 or not getattr(self.comm, "fused", False):
+            return None
+        from . import _native as N
+        return self.comm.hop(N.stream_ptr(None, self.eng.device))
+
     def _send_boundary(self):
-        if self.rank == self.world - 1:
+        if self.rank == self.world - 1 or getattr(self.comm, "fused", False):
             return
         L = self.local_slices
         self.comm.send(self.eng.U[:, L].contiguous(), dst=self.rank + 1)
@@ -147,7 +272,11 @@ class ShardedParareal:
 
     def coarse_init(self) -> None:
         self._recv_boundary()
-        self.eng.coarse_range(0, 0, self.local_slices)
+        hop = self._hop()
+        if hop is None:
+            self.eng.coarse_range(0, 0, self.local_slices)
+        else:
+            self.eng.coarse_range(0, 0, self.local_slices, hop=hop)
         self._send_boundary()
         self.eng.changed.fill_(1)        # every F(U_n^0) is needed at k = 0
         self.k = 0
@@ -183,13 +312,16 @@ class ShardedParareal:
             eng.changed[:, 0] = (eng.changed[:, 0] & 2) | (1 if force_all else 0)
         elif force_all:
             eng.changed[:, 0] |= 1
+        hop = self._hop()
         if coarse_chunks is None:
-            eng.coarse_range(1, 0, self.local_slices)
-        else:
-            for n0, n1 in coarse_chunks:
+            coarse_chunks = [(0, self.local_slices)]
+        for c, (n0, n1) in enumerate(coarse_chunks):
+            if hop is not None and c == len(coarse_chunks) - 1:
+                eng.coarse_range(1, n0, n1, hop=hop)       # the last range hands U_{s1} on
+            else:
                 eng.coarse_range(1, n0, n1)
-                if on_coarse_chunk is not None:
-                    on_coarse_chunk(n0, n1)
+            if on_coarse_chunk is not None:
+                on_coarse_chunk(n0, n1)
         self._send_boundary()
         eng.check_status()
         return eng.inc.clone()
@@ -403,12 +535,27 @@ class SimulatedRanks:
     exercised on one GPU, with no kernels waiting on one another."""
 
     def __init__(self, grid, fine, coarse, num_slices: int, fine_steps: int, world: int, *,
-                 batch: int = 1, inc_tol: float = 1e-10, engine_factory=None, device=None):
-        hub = LoopbackComm(world)
+                 batch: int = 1, inc_tol: float = 1e-10, engine_factory=None, device=None,
+                 hop: bool = False):
+        """``hop``: hand the boundaries over with the device-initiated hop (HopComm over
+        plain device addresses: fused stores + flag from the coarse sweep, stream wait and
+        take on the receiving shard) instead of mailbox copies."""
+        if hop:
+            import torch
+
+            from . import _native as N
+            dev = torch.device(device) if device is not None else torch.device(
+                "cuda", torch.cuda.current_device())
+            ctx = N.Context.get(dev.index if dev.index is not None else torch.cuda.current_device())
+            comms = HopComm.loopback(ctx, world, batch, grid.device_size)
+            self._boxes = [c.box for c in comms]
+        else:
+            hub = LoopbackComm(world)
+            comms = [hub.view(r) for r in range(world)]
         self.shards = [ShardedParareal(grid, fine, coarse, num_slices, fine_steps, rank=r,
                                        world=world, engine_factory=engine_factory,
                                        inc_tol=inc_tol, device=device, batch=batch,
-                                       comm=hub.view(r))
+                                       comm=comms[r])
                        for r in range(world)]
         self.world, self.B = world, batch
         self.N = num_slices

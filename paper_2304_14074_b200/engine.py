@@ -113,15 +113,19 @@ class PararealEngine:
         m = self.grid.interior_per_axis
         return (m,) if self.grid.dim == 1 else (m, self.grid.pitch)
 
-    def coarse_range(self, mode: int, n0: int, n1: int):
-        """chp_coarse_sweep over local slices [n0, n1) (no host sync)."""
-        self._coarse(mode, n0, n1)
+    def coarse_range(self, mode: int, n0: int, n1: int, hop=None):
+        """chp_coarse_sweep over local slices [n0, n1) (no host sync).  ``hop``: an
+        ``_native.ChpHop`` -- the sweep also hands U[n1] to the next rank's mailbox
+        (chp_coarse_sweep_hop: fused into the cooperative kernel where there is one)."""
+        self._coarse(mode, n0, n1, hop)
 
-    def _coarse(self, mode: int, n0: int, n1: int):
-        st = self.ctx.L.chp_coarse_sweep(
+    def _coarse(self, mode: int, n0: int, n1: int, hop=None):
+        import ctypes
+        st = self.ctx.L.chp_coarse_sweep_hop(
             self.ctx.h, self._native_grid(), self.coarse.native(), mode, self.B, self.N, n0, n1,
             N.ptr(self.U), N.ptr(self.F), N.ptr(self.G), (self.N + 1) * self.fs, self.fs,
-            N.ptr(self.changed), N.ptr(self.inc), N.ptr(self.info_coarse), N.stream_ptr(None, self.device))
+            N.ptr(self.changed), N.ptr(self.inc), N.ptr(self.info_coarse),
+            ctypes.byref(hop) if hop is not None else None, N.stream_ptr(None, self.device))
         self.ctx.check(st, "chp_coarse_sweep")
 
     def _raise(self, info_t, spec, labels=None):

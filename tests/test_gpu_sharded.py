@@ -29,17 +29,22 @@ def _single(P, G, g, var, part, eps, u0s, max_iter):
     return eng
 
 
-def _sharded(P, G, D, g, var, part, eps, u0s, world, max_iter):
+def _sharded(P, G, D, g, var, part, eps, u0s, world, max_iter, hop=False):
     f, c = P.propagator_pair(P.AlgorithmVariant(var), part, eps)
-    sim = D.SimulatedRanks(g, f, c, part.num_slices, part.fine_steps, world, batch=len(u0s))
+    sim = D.SimulatedRanks(g, f, c, part.num_slices, part.fine_steps, world, batch=len(u0s),
+                           hop=hop)
     sim.load([G.Field(g, u) for u in u0s])
     sim.run(max_iter=max_iter)
     return sim
 
 
 @pytest.mark.parametrize("case", ["c3_trunc", "c5_trunc", "c2_trunc_batch"])
-@pytest.mark.parametrize("world", [2, 4])
-def test_simulated_ranks_bit_identical(M, case, world):
+@pytest.mark.parametrize("world,hop", [(2, False), (4, False), (2, True), (4, True)])
+def test_simulated_ranks_bit_identical(M, case, world, hop):
+    """hop=True: the boundaries travel by the device-initiated hop of include/chp.h chp_hop
+     -- stores fused into the cooperative 2D coarse kernel's last
+    correction (c3/c5) or a put kernel after the 1D sweep (c2), flag release, stream wait,
+    take and ack -- instead of mailbox copies; still bit-identical."""
     P, G, D = M
     if case == "c3_trunc":        # config 3's grid, eps, dt, dT and u0; first 8 slices
         c = O.CONFIGS[3]
@@ -60,7 +65,7 @@ def test_simulated_ranks_bit_identical(M, case, world):
         part, eps, var = P.TimePartition(8 * dT, 8, c["J"]), c["eps"], "npa1"
         u0s, max_iter = [O.initial_condition(2, b) for b in range(3)], 10
     one = _single(P, G, g, var, part, eps, u0s, max_iter)
-    sim = _sharded(P, G, D, g, var, part, eps, u0s, world, max_iter)
+    sim = _sharded(P, G, D, g, var, part, eps, u0s, world, max_iter, hop)
     sh0 = sim.shards[0]
     conv = sh0.converged
     assert conv == one.converged_at

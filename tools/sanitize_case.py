@@ -23,4 +23,7 @@ P.run(Field(g2, rng.uniform(-0.05, 0.05, g2.interior_count)), P.AlgorithmVariant
       P.TimePartition(0.02, 4, 4), 0.05, stop="increment")
 g3 = SpatialGrid(2, 129)
 S.propagate(Field(g3, rng.uniform(-0.5, 0.5, g3.interior_count)), S.PropagatorSpec(S.Scheme.LINEAR_B, 1e-4, 0.02), 2)
+# N = 1024: bulk-copy row fill, TMA tile fill and TMA store of the column pass
+g4 = SpatialGrid(2, 1025)
+S.propagate(Field(g4, rng.uniform(-0.5, 0.5, g4.interior_count)), S.PropagatorSpec(S.Scheme.LINEAR_B, 1e-5, 0.01), 2)
 print("sanitize cases done")
