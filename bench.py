@@ -267,7 +267,7 @@ def run_gpu(args):
         return
     peaks, src = measured_peaks()
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             traffic = json.load(f)["fine_step_bytes_per_grid_point_step"]
     except (OSError, KeyError, ValueError):
         traffic = None
@@ -281,6 +281,10 @@ def run_gpu(args):
         "data": "synthetic (seeded config-5 initial condition, SURVEY.md 8(d))",
         "config": {"workload": "config5: 2D 1023^2 PA3 eps=0.01 T=2 N=512 J=256, every slice "
                                "active each step", "parallelism": f"time-slices x{world}",
+                   "coarse_chain_hop": ("none (one rank)" if world == 1 else
+                                        "device-initiated hop over cudaIpc (CHP_HOP=ipc)"
+                                        if os.environ.get("CHP_HOP", "") == "ipc"
+                                        else "torch.distributed send/recv (NCCL)"),
                    "l2": "working set 13 GB >> 126 MB L2 (no flush needed)"},
         "fine_phase": {"ms": fine_ms, "grid_point_steps_per_s": local_pts / (fine_ms * 1e-3)},
         "coarse_init_s": init_s,

@@ -221,7 +221,15 @@ class ShardedParareal:
         self.incs: list = []              # per-iteration [B] increments
         self._torch = torch
         self._pending = []              # deferred increment reductions (iterate(defer=True))
-        self.comm = comm if comm is not None else TorchComm(rank, world)
+        if comm is None:
+            # CHP_HOP=ipc: boundaries by the device-initiated hop over cudaIpc mailboxes
+            # (one process per GPU on one node) instead of dist.send/recv
+            import os
+            if world > 1 and os.environ.get("CHP_HOP", "") == "ipc":
+                comm = HopComm.over_ipc(self.eng.ctx, rank, world, self.B, self.eng.fs)
+            else:
+                comm = TorchComm(rank, world)
+        self.comm = comm
 
     # -- batch-1 views of the reference-shaped results -------------------------
     @property
