@@ -925,7 +925,8 @@ bool make_qmap(CUtensorMap* map, double* Qb, int nsys) {
   const cuuint32_t estr[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, Qb, dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CT::IB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CT::IB == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                          : (CT::IB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -939,10 +940,11 @@ bool make_pmap(CUtensorMap* map, double* P, int nsys) {
   const cuuint64_t rp = (cuuint64_t)2 * N * sizeof(double);   // bytes per row pair
   const cuuint64_t dims[3] = {(cuuint64_t)2 * N, (cuuint64_t)F::L * (cuuint64_t)nsys, (cuuint64_t)F::C};
   const cuuint64_t strides[2] = {rp * F::C, rp};
-  const cuuint32_t box[3] = {16, (cuuint32_t)F::L, (cuuint32_t)F::C};
+  const cuuint32_t box[3] = {(cuuint32_t)(linb::ColT<N>::PB / 8), (cuuint32_t)F::L, (cuuint32_t)F::C};
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, P, dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             linb::ColT<N>::PB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -967,9 +969,11 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
     if constexpr (N >= 64)
       cudaFuncSetAttribute(linb::k2d_colt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)linb::ColT<N>::SMEM);
-    if constexpr (N == 1024)
-      cudaFuncSetAttribute(linb::k2d_colt2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)linb::ColT2<N>::SMEM);
+    if constexpr (N == 1024) {
+      if constexpr (linb::ColT<N>::PB == 128)
+        cudaFuncSetAttribute(linb::k2d_colt2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)linb::ColT2<N>::SMEM);
+    }
     attrs = true;
   }
   const long long fs2 = (long long)N * N;
@@ -1006,12 +1010,14 @@ cudaError_t run_linear_b2(const chp_grid& g, const chp_spec& sp, int steps, int 
     if constexpr (N >= 64) {
       if (tma) {
         if constexpr (N == 1024) {
+          if constexpr (linb::ColT<N>::PB == 128) {
           // measured slower (kernel bench 17.08 vs 14.53 ms per 16 config-5-shaped steps): off by default
           static const bool teams = [] { const char* e = getenv("CHP_COL_TEAMS"); return e && e[0] == '1'; }();
           if (teams) {
             linb::k2d_colt2<N><<<dim3(cgrid.x / 2, cgrid.y), linb::ColT2<N>::THREADS, linb::ColT2<N>::SMEM, st>>>(
                 qmap, pmap, ca);
             return;
+          }
           }
         }
         linb::k2d_colt<N><<<cgrid, CG::THREADS, linb::ColT<N>::SMEM, st>>>(qmap, pmap, ca);

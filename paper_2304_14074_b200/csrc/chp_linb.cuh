@@ -30,17 +30,21 @@
 #include <cuda.h>            // CUtensorMap (type only; the encoder is resolved at run time)
 #include "chp_fdst.cuh"
 
+// N = 1024 block shapes: 2 warps (2 lane groups) per block, 4 blocks per SM.  The same 8
+// warps per SM as 4 x 2, but the groups that move in lockstep behind one block's barriers and
+// tile are half as many and four independent blocks interleave their load / transform / store
+// phases: 13.90 vs 14.15 ms per 16 config-5-shaped steps (profiles/r02_linb_ab.md).
 #ifndef CHP_ROW_WARPS
-#define CHP_ROW_WARPS 4
+#define CHP_ROW_WARPS 2
 #endif
 #ifndef CHP_ROW_MINB
-#define CHP_ROW_MINB 2
+#define CHP_ROW_MINB 4
 #endif
 #ifndef CHP_COL_WARPS
-#define CHP_COL_WARPS 4
+#define CHP_COL_WARPS 2
 #endif
 #ifndef CHP_COL_MINB
-#define CHP_COL_MINB 2
+#define CHP_COL_MINB 4
 #endif
 
 namespace linb {
@@ -464,17 +468,22 @@ template <int N> struct ColT {          // TMA column pass geometry
   static constexpr size_t REGIONS = sizeof(double2) * (size_t)(CG::RBASE(CG::GALL - 1) + F::RS);
   // lane 0's mirror of n = 0 reads row N (one row past the tile; the value is discarded)
   static constexpr size_t SMEM = 1024 + (TILE + IB > REGIONS ? TILE + IB : REGIONS);
-  static_assert(N >= 64 && CG::GROUPS == CG::GALL && (IB == 64 || IB == 128), "TMA column pass geometry");
+  static_assert(N >= 64 && CG::GROUPS == CG::GALL && (IB == 32 || IB == 64 || IB == 128),
+                "TMA column pass geometry");
   // 16-byte chunk XOR of the hardware swizzle for tile row r (64B: bits 7-8 of the byte
   // offset = (r >> 1) & 3; 128B: bits 7-9 = r & 7)
-  CHP_DEV static int swz(int r) { return IB == 64 ? ((r >> 1) & 3) : (r & 7); }
+  // (32B: bit 7 = (r >> 2) & 1)
+  CHP_DEV static int swz(int r) { return IB == 32 ? ((r >> 2) & 1) : (IB == 64 ? ((r >> 1) & 3) : (r & 7)); }
   // P leaves through one TMA store (UTMASTG) when the block's pairs span 128 bytes of a P
   // row pair (GROUPS = 4: N = 1024): the inverse transform's outputs are staged in a
   // 128-byte-swizzled tile [j][l][128 B] (row pair k = C l + j at tile row j L + l, so the
   // 32 lanes of a store instruction hit 32 consecutive tile rows: conflict free), and the
   // tensor map's dimension order {columns, l, j} scatters the tile rows to P's row pairs
-  static constexpr bool PSTORE = (GROUPS == 4);
-  static constexpr size_t PTILE = (size_t)(N / 2) * 128;
+  // (GROUPS = 2: 64-byte tile rows with the 64-byte swizzle, XOR term (row >> 1) & 3)
+  static constexpr bool PSTORE = (GROUPS == 4 || GROUPS == 2);
+  static constexpr int PB = 32 * GROUPS;                  // P tile row bytes: 128 or 64
+  static constexpr size_t PTILE = (size_t)(N / 2) * PB;
+  CHP_DEV static int pswz(int l) { return PB == 128 ? (l & 7) : ((l >> 1) & 3); }
 };
 
 // loader of the forward transform: column pair g of the swizzled tile.  Rows l + L n2 and
@@ -536,13 +545,13 @@ k2d_colt(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUten
     // P (pair-interleaved): rows (2k, 2k+1), columns (2 kq, 2 kq + 1), k = C l + j
     if constexpr (CT::PSTORE) {
       // tile row j L + l, 16-byte chunks 2g and 2g + 1, XOR-swizzled with the row's low bits
-      unsigned char* pt = tile + l * 128;
-      const int c0 = ((2 * g) ^ (l & 7)) << 4, c1 = ((2 * g + 1) ^ (l & 7)) << 4;
+      unsigned char* pt = tile + l * CT::PB;
+      const int c0 = ((2 * g) ^ CT::pswz(l)) << 4, c1 = ((2 * g + 1) ^ CT::pswz(l)) << 4;
       fdst::pair_dst_ld<N, false, false, fdst::BlockSync<false, true>>(
           fdst::SmemLd<N>(reg, l), reg, twl, l, sa2, ca2,
           [&](int j, double a0, double a1, double b0, double b1) {
-            *reinterpret_cast<double2*>(pt + j * (L * 128) + c0) = make_double2(a0, a1);
-            *reinterpret_cast<double2*>(pt + j * (L * 128) + c1) = make_double2(b0, b1);
+            *reinterpret_cast<double2*>(pt + j * (L * CT::PB) + c0) = make_double2(a0, a1);
+            *reinterpret_cast<double2*>(pt + j * (L * CT::PB) + c1) = make_double2(b0, b1);
           });
       fence_async_proxy();
       __syncthreads();
@@ -570,7 +579,7 @@ template <int N> struct ColT2 {
   static constexpr int THREADS = 2 * ColG<N>::THREADS;
   static constexpr size_t TEAM = ((CT::SMEM - 1024) + 1023) / 1024 * 1024;   // per-team bytes
   static constexpr size_t SMEM = 1024 + 2 * TEAM;
-  static_assert(CT::PSTORE, "two-team column pass: N = 1024 geometry");
+  static_assert(CT::PSTORE && CT::PB == 128, "two-team column pass: N = 1024, 4-pair tiles");
 };
 
 template <int N>

@@ -75,3 +75,43 @@ def test_simulated_ranks_bit_identical(M, case, world, hop):
     assert np.array_equal(inc_one, inc_sim)
     for i in range(len(u0s)):
         assert np.array_equal(sim.iterates(i), one.iterates_host(i)), i
+
+
+@pytest.mark.parametrize("dim", [1, 2])
+def test_chunked_sweeps_bit_identical_on_device(M, dim):
+    """chunked fine/coarse sweeps (the e2e step's copy pipelining) against one
+    sweep on the DEVICE engine (k1d_coarse_sweep / k2d_coarse2): the increment accumulates
+    across the chunk launches and the changed flag of the first slice of a chunk survives
+    between them, so U, G, changed and the increments must be bit-identical."""
+    import torch
+    P, G, D = M
+    if dim == 1:
+        g = G.SpatialGrid(1, 129)
+        part, eps = P.TimePartition(0.08, 8, 16), 0.05
+        u0 = 0.1 * np.sin(2 * np.pi * np.arange(1, 128) / 128) + \
+            np.random.default_rng(3).uniform(-0.01, 0.01, 127)
+    else:
+        g = G.SpatialGrid(2, 65)
+        part, eps = P.TimePartition(0.04, 8, 8), 0.03
+        u0 = np.random.default_rng(4).uniform(-0.05, 0.05, g.interior_count)
+    f, c = P.propagator_pair(P.AlgorithmVariant.PA3, part, eps)
+
+    def run(chunked):
+        sh = D.ShardedParareal(g, f, c, part.num_slices, part.fine_steps)
+        sh.load(G.Field(g, u0))
+        sh.coarse_init()
+        incs = []
+        for _ in range(4):
+            if chunked:
+                incs.append(sh.iterate(fine_chunks=[(0, 3, None), (3, 8, None)],
+                                       coarse_chunks=[(0, 2), (2, 5), (5, 8)]))
+            else:
+                incs.append(sh.iterate())
+        torch.cuda.synchronize()
+        e = sh.eng
+        return (e.U.cpu().numpy().copy(), e.G.cpu().numpy().copy(),
+                e.changed.cpu().numpy().copy(), np.array(incs))
+
+    a, b = run(False), run(True)
+    for x, y, name in zip(a, b, ("U", "G", "changed", "increments")):
+        assert np.array_equal(x, y), name
