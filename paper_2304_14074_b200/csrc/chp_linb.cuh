@@ -30,15 +30,15 @@
 #include <cuda.h>            // CUtensorMap (type only; the encoder is resolved at run time)
 #include "chp_fdst.cuh"
 
-// N = 1024 block shapes: 2 warps (2 lane groups) per block, 4 blocks per SM.  The same 8
-// warps per SM as 4 x 2, but the groups that move in lockstep behind one block's barriers and
-// tile are half as many and four independent blocks interleave their load / transform / store
-// phases: 13.90 vs 14.15 ms per 16 config-5-shaped steps (profiles/r02_linb_ab.md).
+// N = 1024 block shapes (profiles/r02_linb_ab.md): row pass 4 warps x 2 blocks per SM (a 5-slot
+// ring: fewer chunks per strip and fewer block barriers than 2 x 4), column pass 2 warps x 4
+// blocks per SM (2-pair tiles: four independent blocks interleave their tile load / transform /
+// store phases where two 4-warp blocks left the SM waiting on both tiles at once).
 #ifndef CHP_ROW_WARPS
-#define CHP_ROW_WARPS 2
+#define CHP_ROW_WARPS 4
 #endif
 #ifndef CHP_ROW_MINB
-#define CHP_ROW_MINB 4
+#define CHP_ROW_MINB 2
 #endif
 #ifndef CHP_COL_WARPS
 #define CHP_COL_WARPS 2
@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
   if (a.mode == MODE_MID) Pin = a.in + (long long)sys * a.in_stride;
   else U = a.in + (a.in_index ? (long long)a.in_index[sys] : (long long)sys) * a.in_stride;
 
+  double2 xo[R];                                               // the group's own x pair (phase 0 -> 1)
   for (int t = 0; t < chunks; ++t) {
     const int p0 = sp0 + t * G;
     // ---- phase 0: slot of pair s0 = p0 + g holds x rows (2 s0, 2 s0 + 1) ----
@@ -278,11 +279,15 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
           for (int i = 0; i < R; ++i) reg[l + L * i] = make_double2(0.0, 0.0);
         }
         __syncwarp();
+        // x goes to the slot for the neighbouring group (its rows A, B) and stays in this
+        // lane's registers for the group's own phase 1 (rows C, D): lane chunk n = R l + i
         double2* ob = fdst::out_base<N>(reg, l);
         fdst::pair_dst_ld<N>(PlainLd<N>(reg, l), reg, twl, l, sa2, ca2,
                              [&](int j, double a0, double a1, double b0, double b1) {
-          ob[2 * j] = make_double2(a0, b0);
-          ob[2 * j + 1] = make_double2(a1, b1);
+          xo[2 * j] = make_double2(a0, b0);
+          xo[2 * j + 1] = make_double2(a1, b1);
+          ob[2 * j] = xo[2 * j];
+          ob[2 * j + 1] = xo[2 * j + 1];
         });
       } else {
         // first step: x is the physical input (storage row i-1 = math row i)
@@ -297,6 +302,8 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
           }
           reg[l + L * i + i / Q] = make_double2(xa, xb);
         }
+#pragma unroll
+        for (int i = 0; i < R; ++i) xo[i] = make_double2(0.0, 0.0);   // defined on every path: never live across a chunk
       }
     }
     __syncthreads();
@@ -305,41 +312,53 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
     const bool act = s1 >= sp0 && s1 < sp1;
     double2* r0 = slots + ((t * G + g + SL - 1) % SL) * RS;   // pair s1: rows 2s1, 2s1+1
     const double2* r1 = slots + ((t * G + g) % SL) * RS;      // pair s1+1: rows 2s1+2, 2s1+3
-    double2 rhs[R];                                            // lane chunk n = R l + i
     {
-      const int nb = R * l;
-      const double2* u0 = r0 + (R + 1) * l;                    // p2(R l + i) = (R+1) l + i
-      const double2* u1 = r1 + (R + 1) * l;
-      // left neighbour (n = nb - 1) and right neighbour (n = nb + R)
-      double2 ul = make_double2(0.0, 0.0), vl = make_double2(0.0, 0.0);
-      if (l > 0) { ul = u0[-2]; vl = u1[-2]; }
-      double2 ur = make_double2(0.0, 0.0), vr = make_double2(0.0, 0.0);
-      if (l < L - 1) { ur = u0[R + 1]; vr = u1[R + 1]; }
-      // rows: A = 2s1 (u.x), B = 2s1+1 (u.y), Cc = 2s1+2 (v.x), D = 2s1+3 (v.y)
-      double wBl = wcub(ul.y), wCl = wcub(vl.x);
-      double2 u = u0[0], v = u1[0];
+      double2* u0 = r0 + (R + 1) * l;                          // p2(R l + i) = (R+1) l + i
+      if (a.mode != MODE_MID) {
+        // first step: x was loaded straight into the slots; pick up the group's own pair
+        // before the neighbouring group rewrites that slot in place
+        const double2* u1 = r1 + (R + 1) * l;
+#pragma unroll
+        for (int i = 0; i < R; ++i) xo[i] = u1[i];
+        __syncthreads();
+      }
+      // Rows A = 2s1, B = 2s1+1 come from the neighbouring group's slot r0, rows C = 2s1+2,
+      // D = 2s1+3 are this group's own pair, still in registers (xo).  Left neighbour
+      // (n = R l - 1) and right neighbour (n = R l + R): r0's through shared memory, the own
+      // pair's from the adjacent lanes' registers.  Nobody else touches r0 in this phase, so the
+      // rhs replaces x in place as the sweep goes (after every lane's edge reads).
+      double2 ul = make_double2(0.0, 0.0), ur = make_double2(0.0, 0.0);
+      if (l > 0) ul = u0[-2];
+      if (l < L - 1) ur = u0[R + 1];
+      double vlx = __shfl_up_sync(0xffffffffu, xo[R - 1].x, 1, L);
+      double vrx = __shfl_down_sync(0xffffffffu, xo[0].x, 1, L);
+      if (l == 0) vlx = 0.0;
+      if (l == L - 1) vrx = 0.0;
+      __syncwarp();
+      double wBl = wcub(ul.y), wCl = wcub(vlx);
+      double2 u = u0[0], v = xo[0];
       double wB = wcub(u.y), wC = wcub(v.x);
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        double2 un, vn;
-        if (i + 1 < R) { un = u0[i + 1]; vn = u1[i + 1]; }
-        else { un = ur; vn = vr; }
-        const double wBr = wcub(un.y), wCr = wcub(vn.x);
+        double2 un;
+        double vnx;
+        if (i + 1 < R) { un = u0[i + 1]; vnx = xo[i + 1].x; }
+        else { un = ur; vnx = vrx; }
+        const double wBr = wcub(un.y), wCr = wcub(vnx);
         const double wA = wcub(u.x), wD = wcub(v.y);
         // L w at (B, n) and (C, n): up + down + left + right - 4 centre, times dt/h^2
         const double sB = fma(-4.0, wB, ((wA + wC) + (wBl + wBr)));
         const double sC = fma(-4.0, wC, ((wB + wD) + (wCl + wCr)));
-        rhs[i] = make_double2(fma(cdt, sB, u.y), fma(cdt, sC, v.x));
+        u0[i] = make_double2(fma(cdt, sB, u.y), fma(cdt, sC, v.x));
         wBl = wB; wCl = wC; wB = wBr; wC = wCr;
-        u = un; v = vn;
+        u = un;
+        if (i + 1 < R) v = xo[i + 1];
+        // keep the x loads of later columns from being hoisted over the whole sweep (their
+        // registers are what the own pair occupies)
+        if ((i & 3) == 3) asm volatile("" ::: "memory");
       }
-      (void)nb;
     }
-    __syncthreads();                                           // every slot's x has been read
     {
-      double2* w0 = r0 + (R + 1) * l;
-#pragma unroll
-      for (int i = 0; i < R; ++i) w0[i] = rhs[i];
       __syncwarp();
       // Q rows 2s1+1 (a) and 2s1+2 (b, absent for the last pair) straight from the
       // post-processing registers (no staging): see qpos for the column-pair order.
