@@ -77,10 +77,15 @@ template <int N> CHP_DEV constexpr int p2(int n) { return n + n / FG<N>::R; }
 // Input loaders of the pre-processing: v(n2) = pair value at n = l + L n2, w(n2) = its
 // mirror at N - n.  SmemLd: a group-private pair region in p2 layout; other loaders
 // (chp_linb.cuh TileLd: the column pass's TMA tile) only change the addressing.
-template <int N> struct SmemLd {
+// PADCOPY (Q == 1 geometries): the writer of the region also stored every element n = R q
+// (q >= 1) into the pad slot in front of it, p2(n) - 1.  Lane 0's mirror values are exactly
+// those elements; reading the copies keeps the 32 lanes of a mirror load on 32 consecutive
+// slots (4 wavefronts) where lane 0 would otherwise sit one slot off and cost a fifth.
+template <int N, bool PADCOPY = false> struct SmemLd {
   const double2 *sd, *sm0, *sm1;
+  static_assert(!PADCOPY || FG<N>::Q == 1, "pad copies: one DFT per lane geometries");
   CHP_DEV SmemLd(const double2* src, int l)
-      : sd(src + l), sm0(src + p2<N>(N - l)),
+      : sd(src + l), sm0(src + p2<N>(N - l) - ((PADCOPY && l == 0) ? 1 : 0)),
         // Q == 2: lane 0's mirror offsets differ by one for odd n2 (see header)
         sm1((FG<N>::Q == 2 && l == 0) ? src + p2<N>(N - l) - 1 : src + p2<N>(N - l)) {}
   CHP_DEV double2 v(int n2) const { return sd[FG<N>::L * n2 + n2 / FG<N>::Q]; }

@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
   // (UBLKCP) on the group's mbarrier; narrower groups (two or more per warp, 4 KB pairs or
   // less) keep the per-thread cp.async fill, which measured faster there
   constexpr bool BULK = (L == 32);
+  constexpr bool PADC = (Q == 1);          // pad copies for the second transform's mirror reads
   __shared__ __align__(8) unsigned long long rbar[G];
   unsigned rphase = 0;
   if (BULK && a.mode == MODE_MID) {
@@ -349,7 +350,9 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
         // L w at (B, n) and (C, n): up + down + left + right - 4 centre, times dt/h^2
         const double sB = fma(-4.0, wB, ((wA + wC) + (wBl + wBr)));
         const double sC = fma(-4.0, wC, ((wB + wD) + (wCl + wCr)));
-        u0[i] = make_double2(fma(cdt, sB, u.y), fma(cdt, sC, v.x));
+        const double2 rh = make_double2(fma(cdt, sB, u.y), fma(cdt, sC, v.x));
+        u0[i] = rh;
+        if (PADC && i == 0 && l > 0) u0[-1] = rh;               // pad copy of the chunk's first column
         wBl = wB; wCl = wC; wB = wBr; wC = wCr;
         u = un;
         if (i + 1 < R) v = xo[i + 1];
@@ -372,7 +375,8 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
       // as the transform has read its last value from the slot (the callbacks run after that)
       const int sn = p0 + G + g;
       const bool prefetch = BULK && a.mode == MODE_MID && t + 1 < chunks && sn <= sp1 && sn < RG::NP;
-      fdst::pair_dst<N>(r0, r0, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
+      fdst::pair_dst_ld<N>(fdst::SmemLd<N, PADC>(r0, l), r0, twl, l, sa2, ca2,
+                           [&](int j, double a0, double a1, double b0, double b1) {
         if ((j & 1) == 0) {
           if (j == 0 && prefetch && l == 0) {
             fence_async_proxy();
@@ -552,10 +556,12 @@ k2d_colt(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUten
   __syncthreads();                                       // the barrier is initialised
   mbar_wait(&bar, 0);
   {
+    constexpr bool PADC = (F::Q == 1);
     double2* ob = fdst::out_base<N>(reg, l);
     auto put = [&](int j, double a0, double a1, double b0, double b1) {
       ob[2 * j] = make_double2(a0, b0);
       ob[2 * j + 1] = make_double2(a1, b1);
+      if (PADC && j == 0 && l > 0) ob[-1] = make_double2(a0, b0);   // pad copy (fdst::SmemLd)
     };
     // D'' of the column pair scales the forward transform's outputs in its post-processing
     fdst::pair_dst_ld<N, false, true, fdst::BlockSync<true, false>>(TileLd<N>(tile, g, l), reg, twl, l, sa2, ca2, put, nullptr,
@@ -567,7 +573,7 @@ k2d_colt(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUten
       unsigned char* pt = tile + l * CT::PB;
       const int c0 = ((2 * g) ^ CT::pswz(l)) << 4, c1 = ((2 * g + 1) ^ CT::pswz(l)) << 4;
       fdst::pair_dst_ld<N, false, false, fdst::BlockSync<false, true>>(
-          fdst::SmemLd<N>(reg, l), reg, twl, l, sa2, ca2,
+          fdst::SmemLd<N, PADC>(reg, l), reg, twl, l, sa2, ca2,
           [&](int j, double a0, double a1, double b0, double b1) {
             *reinterpret_cast<double2*>(pt + j * (L * CT::PB) + c0) = make_double2(a0, a1);
             *reinterpret_cast<double2*>(pt + j * (L * CT::PB) + c1) = make_double2(b0, b1);
@@ -580,7 +586,8 @@ k2d_colt(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUten
       }
     } else {
       double* pl = Ps + ((long long)(F::C * l) * N + 2 * kq) * 2;
-      fdst::pair_dst<N>(reg, reg, twl, l, sa2, ca2, [&](int j, double a0, double a1, double b0, double b1) {
+      fdst::pair_dst_ld<N>(fdst::SmemLd<N, PADC>(reg, l), reg, twl, l, sa2, ca2,
+                           [&](int j, double a0, double a1, double b0, double b1) {
         st256(pl + (long long)j * (2 * N), a0, a1, b0, b1);
       });
     }
