@@ -398,6 +398,10 @@ CHP_DEV void gbar(GridBar& b) {
     __threadfence();
   }
   __syncthreads();
+#ifdef CHP_C2_FT
+  if (b.trace && blockIdx.x == 0 && threadIdx.x == 0 && (int)b.gen < b.cap)
+    b.trace[4096 + 8 * b.gen] = (unsigned long long)clock64();
+#endif
 }
 
 // fixed-order block reduction of (v0..v3) into part[blockIdx][0..3]
@@ -422,12 +426,32 @@ CHP_DEV void coop_block_partials(double (&v)[K], double* red, double* part) {
 template <int K>
 CHP_DEV void coop_total(const double* part, double* red, double (&out)[K]) {
   if (threadIdx.x < 32) {
+    // same summation order as a per-k loop (b = lane, lane + 32, ...), with the loads
+    // of eight blocks' K partials in flight together
+    double x[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) x[k] = 0.0;
+    for (int b0 = threadIdx.x; b0 < (int)gridDim.x; b0 += 32 * 8) {
+      double v[8][K];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int b = b0 + 32 * e;
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[e][k] = (b < (int)gridDim.x) ? part[b * 8 + k] : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (b0 + 32 * e < (int)gridDim.x) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) x[k] += v[e][k];
+        }
+      }
+    }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      double x = 0.0;
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) x += part[b * 8 + k];
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (threadIdx.x == 0) red[k] = x;
+      double y = x[k];
+      for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+      if (threadIdx.x == 0) red[k] = y;
     }
   }
   __syncthreads();
@@ -1104,7 +1128,10 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
     {
       static unsigned long long* tr = nullptr;
       const char* env = getenv("CHP_COOP_TRACE");
-      if (env && !tr) cudaMalloc(&tr, sizeof(unsigned long long) * 4096);
+      if (env && !tr) {
+        cudaMalloc(&tr, sizeof(unsigned long long) * 4096 * 9);
+        cudaMemset(tr, 0, sizeof(unsigned long long) * 4096 * 9);
+      }
       ca.trace = env ? tr : nullptr;
       ca.trace_cap = 4096;
       if (env) g_coop_trace = tr;
@@ -1220,7 +1247,7 @@ cudaError_t chp2d_coarse_sweep(Chp2d* c, const chp_grid& g, const chp_spec& sp, 
 // debug: copy the cooperative coarse kernel's barrier timestamps (ns) to the host
 extern "C" int chp_debug_trace(unsigned long long* host, int n) {
   if (!g_coop_trace || !host || n <= 0) return 0;
-  if (n > 4096) n = 4096;
+  if (n > 4096 * 9) n = 4096 * 9;
   cudaMemcpy(host, g_coop_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
   return n;
 }

@@ -319,6 +319,11 @@ chp_status chp_coarse_sweep_hop(chp_ctx* c, const chp_grid* g, const chp_spec* s
     if (e != cudaSuccess) return cuda_fail(c, e, "chp1d_coarse_sweep");
     return hop ? put() : CHP_OK;
   }
+  // the 2D kernels move fields as 16-byte words (rows are N = m + 1 doubles, N even)
+  auto odd16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0; };
+  if (odd16(U) || odd16(G) || (F && odd16(F)) || (ic_stride & 1) || (sl_stride & 1) ||
+      (hop && (odd16(hop->peer_u) || (hop->peer_stride & 1))))
+    return fail(c, CHP_ERR_ARG, "2D fields must be 16-byte aligned with even strides");
   bool fused = false;
   cudaError_t e = chp2d_coarse_sweep(c->d2, *g, *sp, mode, nic, nsl, n0, n1, U, F, G, ic_stride,
                                      sl_stride, changed, inc, info, st, &why, hop, &fused);

@@ -126,7 +126,9 @@ struct PhaseTick {
   CHP_DEV static void z_read() { tick(); }
 };
 
-template <int N, bool DS = false, bool PS = false, class Sy = WarpSync, class Ld, class Out>
+// DS: 0 no input scale; 1 scale table in global memory (read with ld.global.cg); 2 scale
+// table anywhere (plain loads: a copy staged in shared memory).
+template <int N, int DS = 0, bool PS = false, class Sy = WarpSync, class Ld, class Out>
 CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restrict__ twl, int l,
                       double sa2, double ca2, Out out,
                       const double2* __restrict__ dsc = nullptr,
@@ -147,7 +149,8 @@ CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restr
     double2 v = ld.v(n2);
     double2 w = ld.w(n2);
     if constexpr (DS) {
-      const double2 dv = __ldcg(dsc + L * n2), dw = __ldcg(dsm - L * n2);
+      const double2 dv = (DS == 2) ? dsc[L * n2] : __ldcg(dsc + L * n2);
+      const double2 dw = (DS == 2) ? dsm[-L * n2] : __ldcg(dsm - L * n2);
       v = make_double2(v.x * dv.x, v.y * dv.y);
       w = make_double2(w.x * dw.x, w.y * dw.y);
     }
@@ -248,7 +251,7 @@ CHP_PAIR_ATTR void pair_dst_ld(const Ld ld, double2* reg, const double2* __restr
 }
 
 // Pair DST-I of the pair vector held in `src` (p2 layout, group-private, may alias `reg`).
-template <int N, bool DS = false, bool PS = false, class Out>
+template <int N, int DS = 0, bool PS = false, class Out>
 CHP_PAIR_ATTR void pair_dst(const double2* src, double2* reg, const double2* __restrict__ twl, int l,
                       double sa2, double ca2, Out out,
                       const double2* __restrict__ dsc = nullptr,

@@ -162,14 +162,30 @@ __global__ void __launch_bounds__(128, 2) k_pcg2_cols(Pcg2 a, const double* in, 
   const double2 ac = __ldg(&a.wtab[l]);
   const double2* twl = a.wtab + N + l;
   double2* reg = smp + G2::RBASE(g);
-#pragma unroll 8
-  for (int idx = threadIdx.x; idx < (N / 2) * GROUPS; idx += G2::THREADS) {
-    const int s = idx / GROUPS, c = idx % GROUPS;
-    const double2* src = reinterpret_cast<const double2*>(ins + ((long long)s * N + j0 + 2 * c) * 2);
-    const double2 u = src[0], w = src[1];
-    double2* rg = smp + G2::RBASE(c);
-    rg[fdst::p2<N>(2 * s)] = make_double2(u.x, w.x);
-    rg[fdst::p2<N>(2 * s + 1)] = make_double2(u.y, w.y);
+  // (kFB items' loads are issued together, ahead of the shared-memory stores)
+  constexpr int kFB = 8, kItems = (N / 2) * GROUPS;
+  for (int i0 = threadIdx.x; i0 < kItems; i0 += kFB * G2::THREADS) {
+    double2 u[kFB], w[kFB];
+#pragma unroll
+    for (int e = 0; e < kFB; ++e) {
+      const int idx = i0 + e * G2::THREADS;
+      if (idx < kItems) {
+        const int s = idx / GROUPS, c = idx % GROUPS;
+        const double2* src = reinterpret_cast<const double2*>(ins + ((long long)s * N + j0 + 2 * c) * 2);
+        u[e] = src[0];
+        w[e] = src[1];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < kFB; ++e) {
+      const int idx = i0 + e * G2::THREADS;
+      if (idx < kItems) {
+        const int s = idx / GROUPS, c = idx % GROUPS;
+        double2* rg = smp + G2::RBASE(c);
+        rg[fdst::p2<N>(2 * s)] = make_double2(u[e].x, w[e].x);
+        rg[fdst::p2<N>(2 * s + 1)] = make_double2(u[e].y, w[e].y);
+      }
+    }
   }
   __syncthreads();
   double2* ob = fdst::out_base<N>(reg, l);
@@ -195,14 +211,28 @@ __global__ void __launch_bounds__(128, 2) k_pcg2_cols(Pcg2 a, const double* in, 
     }
   } else {
     double* o = out + (long long)sys * NN;
-#pragma unroll 8
-    for (int idx = threadIdx.x; idx < (N / 2) * GROUPS; idx += G2::THREADS) {
-      const int s = idx / GROUPS, c = idx % GROUPS;
-      const double2* rg = smp + G2::RBASE(c);
-      const double2 u = rg[fdst::p2<N>(2 * s)], w = rg[fdst::p2<N>(2 * s + 1)];
-      double2* dst = reinterpret_cast<double2*>(o + ((long long)s * N + j0 + 2 * c) * 2);
-      dst[0] = make_double2(u.x, w.x);
-      dst[1] = make_double2(u.y, w.y);
+    for (int i0 = threadIdx.x; i0 < kItems; i0 += kFB * G2::THREADS) {
+      double2 u[kFB], w[kFB];
+#pragma unroll
+      for (int e = 0; e < kFB; ++e) {
+        const int idx = i0 + e * G2::THREADS;
+        if (idx < kItems) {
+          const int s = idx / GROUPS, c = idx % GROUPS;
+          const double2* rg = smp + G2::RBASE(c);
+          u[e] = rg[fdst::p2<N>(2 * s)];
+          w[e] = rg[fdst::p2<N>(2 * s + 1)];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < kFB; ++e) {
+        const int idx = i0 + e * G2::THREADS;
+        if (idx < kItems) {
+          const int s = idx / GROUPS, c = idx % GROUPS;
+          double2* dst = reinterpret_cast<double2*>(o + ((long long)s * N + j0 + 2 * c) * 2);
+          dst[0] = make_double2(u[e].x, w[e].x);
+          dst[1] = make_double2(u[e].y, w[e].y);
+        }
+      }
     }
   }
 }

@@ -146,3 +146,29 @@ def kernel_split(nx=1025, nsys=64, steps=16):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "split":
     print(json.dumps(kernel_split()), flush=True)
     print(json.dumps(kernel_split(257, 64, 64)), flush=True)
+
+
+def coarse_ft(nx=1025, nsl=2):
+    """Inside-the-phase clock64 stamps of block 0 / thread 0 (library built with -DCHP_C2_FT)."""
+    import ctypes
+    os.environ["CHP_COOP_TRACE"] = "1"
+    from paper_2304_14074_b200 import _native as NN
+    r = coarse_sweep(nx, nsl)
+    n = 4096 * 9
+    buf = (ctypes.c_ulonglong * n)()
+    NN.lib().chp_debug_trace(buf, n)
+    a = np.array(buf[:n], dtype=np.int64)
+    ft = a[4096:].reshape(4096, 8)
+    rows = []
+    for g in range(1, 4095):
+        if ft[g, 0] == 0 or ft[g + 1, 0] == 0:
+            continue
+        st = ft[g]
+        nxt = ft[g + 1, 0]
+        rows.append({"gen": g, "clk": [int(st[k] - st[0]) if st[k] else None for k in range(1, 6)],
+                     "next_exit": int(nxt - st[0])})
+    return {"coarse": r, "phases": rows[40:64]}
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ft":
+    print(json.dumps(coarse_ft()), flush=True)
