@@ -373,6 +373,9 @@ __global__ void k2d_newton_norm(int nsys, const double* partial, double hd, doub
 // ---------------------------------------------------------------------------
 // Grid-wide barrier for the co-resident (cooperative) launch: one relaxed
 // spin per block and one fence on each side, instead of a fence per poll.
+#ifndef CHP_C2_BAR
+#define CHP_C2_BAR 1      // 1: red.release / ld.acquire; 0: fence + relaxed atomic + fence (0.820 vs 0.794 ms per slice)
+#endif
 struct GridBar {
   unsigned int* cnt;
   unsigned int gen;
@@ -388,14 +391,21 @@ CHP_DEV void gbar(GridBar& b) {
   }
   b.gen += 1;
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(b.cnt, 1u);
     const unsigned int target = b.gen * gridDim.x;
     unsigned int v;
+#if CHP_C2_BAR
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(b.cnt), "r"(1u) : "memory");
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(b.cnt) : "memory");
+    } while (v < target);
+#else
+    __threadfence();
+    atomicAdd(b.cnt, 1u);
     do {
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(b.cnt) : "memory");
     } while (v < target);
     __threadfence();
+#endif
   }
   __syncthreads();
 #ifdef CHP_C2_FT
@@ -1096,18 +1106,21 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
   if (sp.scheme == CHP_LINEAR_A) {
     using G2 = Coop2G<N>;
     static int blocks_dev[kMaxDev] = {};
+    static bool res_ok_dev[kMaxDev] = {};
     int& blocks = blocks_dev[cur_dev()];
+    bool& res_ok = res_ok_dev[cur_dev()];
     if (blocks == 0) {
       cudaFuncSetAttribute(k2d_coarse2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)G2::SMEM);
+                           (int)G2::SMEM_RES);
       int dev = 0, sms = 0, per = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2d_coarse2<N>, G2::THREADS, G2::SMEM);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2d_coarse2<N>, G2::THREADS,
+                                                    G2::SMEM_RES);
       // one block per SM: enough lane groups for every row pair, and half the
       // grid-barrier arrivals of two
       blocks = sms;
-      (void)per;
+      res_ok = per >= 1;
     }
     const size_t NN = (size_t)N * N;
     const size_t doubles = 10 * NN + 2 + (size_t)fs + 16 * (size_t)blocks + 16;
@@ -1136,6 +1149,9 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
       ca.trace_cap = 4096;
       if (env) g_coop_trace = tr;
     }
+    // every lane group owns one row pair for the whole solve: r and w stay in shared memory
+    static const bool no_res = getenv("CHP_C2_NORES") != nullptr;
+    ca.res = (!no_res && res_ok && N / 2 <= blocks * G2::GPB) ? 1 : 0;
     cudaMemsetAsync(ca.bar, 0, sizeof(unsigned int), st);
     ca.lam = nt.lam; ca.wtab = nt.wtab;
     if (hop) {
@@ -1145,7 +1161,7 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
     }
     void* args[] = {&ca};
     return cudaLaunchCooperativeKernel((void*)k2d_coarse2<N>, dim3(blocks), dim3(G2::THREADS),
-                                       args, G2::SMEM, st);
+                                       args, ca.res ? G2::SMEM_RES : G2::SMEM, st);
   }
   // g-buffer: nic compact fields (outside the propagate workspaces)
   double* gb = nullptr;

@@ -65,7 +65,7 @@ struct Coop2Args {
   unsigned int* bar;
   const double* lam; const double2* wtab;
   unsigned long long* trace;
-  int trace_cap, pad2_;
+  int trace_cap, res;             // res: r and w resident in shared memory (one row pair per group)
   // fused boundary hand-off (include/chp.h chp_hop): U[n1] of every IC is also stored to
   // the next rank's mailbox by the last slice's correction, then the flag is released
   double* hop_u; long long hop_stride;
@@ -83,7 +83,11 @@ template <int N> struct Coop2G {
   // after the transform regions: one staged c'' column-pair vector (n = 0..N) per group
   static constexpr int CBASE = RBASE(GPB - 1) + F::RS;
   static constexpr int CS = N + 2;
-  static constexpr size_t SMEM = sizeof(double2) * (size_t)(CBASE + (CHP_C2_CTS ? GPB * CS : 0));
+  static constexpr int XBASE = CBASE + (CHP_C2_CTS ? GPB * CS : 0);
+  static constexpr size_t SMEM = sizeof(double2) * (size_t)XBASE;
+  // resident CG vectors (Coop2Args::res): the residual r and w = A u of the row pair a lane
+  // group owns for the whole solve stay in shared memory (N double2 each)
+  static constexpr size_t SMEM_RES = SMEM + sizeof(double2) * (size_t)(GPB * 2 * N);
 };
 
 // One out-of-line copy of each transform variant for the whole kernel: the
@@ -117,18 +121,20 @@ CHP_DEV void c2_rows(const Coop2Args& a, double2* sm, int op, const double* in, 
   const int g = threadIdx.x / L, l = threadIdx.x % L;
   const int gg = g * gridDim.x + blockIdx.x, ngr = gridDim.x * G2::GPB;
   double2* reg = sm + G2::RBASE(g);
+  double2* resR = sm + G2::XBASE + g * 2 * N;   // a.res: the group's r and w rows
+  double2* resW = resR + N;
   const double2* twl = a.wtab + N + l;
   for (int s0 = 0; s0 < N / 2; s0 += ngr) {
     const int s = s0 + gg;
     const bool have = s < N / 2;              // whole warps iterate together
     const long long base = (long long)(have ? s : 0) * N;   // double2 index of the pair row
     if (op == 3 || op == 5) {
-      double2* Rr = reinterpret_cast<double2*>(a.R) + base;
+      double2* Rr = a.res ? resR : reinterpret_cast<double2*>(a.R) + base;
       double2* Xr = reinterpret_cast<double2*>(a.X) + base;
       const double2* Mr = reinterpret_cast<const double2*>(a.Mi) + base;
       double2* Pr = reinterpret_cast<double2*>(a.P) + base;
       double2* Sr = reinterpret_cast<double2*>(a.S) + base;
-      const double2* Wr = reinterpret_cast<const double2*>(a.W) + base;
+      const double2* Wr = a.res ? resW : reinterpret_cast<const double2*>(a.W) + base;
       const double2* Ir = reinterpret_cast<const double2*>(in) + base;
       const double2* Kr = reinterpret_cast<const double2*>(a.SK) + base;
       // the loads of UN elements are issued together, ahead of the stores (which the
@@ -190,10 +196,10 @@ CHP_DEV void c2_rows(const Coop2Args& a, double2* sm, int op, const double* in, 
     __syncwarp();
     C2_FT(a, gen, 2);
     if (op == 4) {
-      const double2* Rr = reinterpret_cast<const double2*>(a.R) + base;
+      const double2* Rr = a.res ? resR : reinterpret_cast<const double2*>(a.R) + base;
       const double2* Mr = reinterpret_cast<const double2*>(a.Mi) + base;
       const double2* Dr = reinterpret_cast<const double2*>(a.Dk) + base;
-      double2* Wr = reinterpret_cast<double2*>(a.W) + base;
+      double2* Wr = a.res ? resW : reinterpret_cast<double2*>(a.W) + base;
       constexpr int UN = (2 * kC2U) < R ? (2 * kC2U) : R;
 #pragma unroll 1
       for (int i0 = 0; i0 < R; i0 += UN) {

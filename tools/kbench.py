@@ -167,7 +167,8 @@ def coarse_ft(nx=1025, nsl=2):
         nxt = ft[g + 1, 0]
         rows.append({"gen": g, "clk": [int(st[k] - st[0]) if st[k] else None for k in range(1, 6)],
                      "next_exit": int(nxt - st[0])})
-    return {"coarse": r, "phases": rows[40:64]}
+    lo = int(os.environ.get("FT_LO", "40"))
+    return {"coarse": r, "phases": rows[lo:lo + int(os.environ.get("FT_N", "24"))]}
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ft":
