@@ -144,6 +144,8 @@ chp_status chp_propagate(chp_ctx* ctx, const chp_grid* g, const chp_spec* spec,
  * entry (1 iff U[n_begin] changed during this sweep).  Bit 1 of
  * changed[i*(N+1)] (slot 0 -- U[0] never changes) freezes IC i: it is skipped.
  * `inc` (device double, nic) is max-accumulated.
+ * 2D grids: the kernels move fields as 16-byte words, so U, F, G (and a hop mailbox)
+ * must be 16-byte aligned and both strides even (CHP_ERR_ARG otherwise).
  */
 chp_status chp_coarse_sweep(chp_ctx* ctx, const chp_grid* g, const chp_spec* coarse,
                             int mode, int nic, int nslices, int n_begin, int n_end,

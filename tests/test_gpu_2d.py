@@ -263,3 +263,26 @@ def test_config5_accuracy_vs_long_double_truth(M, golden):
         assert err <= float(z[f"oracle_dst_{k}_sub8"][0]), (k, err)
         assert err * 10 <= float(z[f"reference_superlu_{k}_sub8"][0]), (k, err)
     assert rel(v1024[::8], z["truth1024_sub8"]) < 1e-9
+
+
+def test_coarse_sweep_rejects_misaligned_fields(M):
+    """The 2D sweep moves fields as 16-byte words: a field buffer that is only 8-byte
+    aligned is refused with CHP_ERR_ARG (ValueError), not read through misaligned loads."""
+    import torch
+    grid, schemes, parareal = M
+    from paper_2304_14074_b200.engine import PararealEngine
+    g = grid.SpatialGrid(2, 33)
+    part = parareal.TimePartition(0.02, 4, 2)
+    f, c = parareal.propagator_pair(parareal.AlgorithmVariant.PA3, part, 0.05)
+    eng = PararealEngine(g, f, c, 4, 2)
+    eng.load([grid.Field(g, np.random.default_rng(0).uniform(-0.05, 0.05, g.interior_count))])
+    good = eng.U
+    buf = torch.zeros(good.numel() + 1, dtype=good.dtype, device=good.device)
+    eng.U = buf[1:].view(good.shape)
+    eng.U.copy_(good)
+    assert eng.U.data_ptr() % 16 == 8
+    with pytest.raises(ValueError, match="16-byte aligned"):
+        eng.coarse_init()
+    eng.U = good
+    eng.coarse_init()                      # the aligned buffer still works
+    assert bool(torch.isfinite(eng.U).all())
