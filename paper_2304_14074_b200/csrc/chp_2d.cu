@@ -723,7 +723,9 @@ cudaError_t pcg_solve2(Chp2d* cx, const chp_grid& g, int nsys, double a, double 
   bool& attrs = attrs_dev[cur_dev()];
   if (!attrs) {
     const int sm = (int)G2::SMEM;
-    cudaFuncSetAttribute(k_pcg2_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pcg2_rows<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pcg2_rows<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_pcg2_rows<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_pcg2_cols<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_pcg2_cols<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_pcg2_cols<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -757,14 +759,14 @@ cudaError_t pcg_solve2(Chp2d* cx, const chp_grid& g, int nsys, double a, double 
   k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 3, 0, 0,
                                            1.0 / ((double)m * m), a);
   k_pcg2_prep<N><<<eg, 256, 0, st>>>(p);
-  k_pcg2_rows<N><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
+  k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
   k_pcg2_cols<N, 0><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
   if (warm) {
     k_pcg2_warm_a<N><<<eg, 256, 0, st>>>(p);
     k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 4, 0, 0, 0, 0);
-    k_pcg2_rows<N><<<rg, G2::THREADS, sm, st>>>(p, p.P, p.Y, 0);
+    k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.P, p.Y, 0);
     k_pcg2_cols<N, 1><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
-    k_pcg2_rows<N><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
+    k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 0);
     k_pcg2_aptail<N><<<eg, 256, 0, st>>>(p, 0);
     k_pcg2_warm_b<N><<<eg, 256, 0, st>>>(p);
     k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 5, tol * tol, 0, 0, 0);
@@ -778,12 +780,19 @@ cudaError_t pcg_solve2(Chp2d* cx, const chp_grid& g, int nsys, double a, double 
   int chunk = cx->last_cg < 4 ? 4 : (cx->last_cg > 32 ? 32 : cx->last_cg);
   for (int it0 = 0; it0 < max_iter + chunk; it0 += chunk, chunk = 4) {
     for (int it = 0; it < chunk; ++it) {
-      k_pcg2_pdir<N><<<eg, 256, 0, st>>>(p);
-      k_pcg2_rows<N><<<rg, G2::THREADS, sm, st>>>(p, p.P, p.Y, 1);
+#if CHP_PCG2_FUSE
+      k_pcg2_rows<N, 1><<<rg, G2::THREADS, sm, st>>>(p, p.P, p.Y, 1);
       k_pcg2_cols<N, 1><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 1);
-      k_pcg2_rows<N><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 1);
+      k_pcg2_rows<N, 2><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 1);
+      k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, G2::RBLK, 1, 0, 0, 0, 0);
+#else
+      k_pcg2_pdir<N><<<eg, 256, 0, st>>>(p);
+      k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.P, p.Y, 1);
+      k_pcg2_cols<N, 1><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 1);
+      k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.Y, p.Y, 1);
       k_pcg2_aptail<N><<<eg, 256, 0, st>>>(p, 1);
       k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 1, 0, 0, 0, 0);
+#endif
       k_pcg2_update<N><<<eg, 256, 0, st>>>(p);
       k2d_cg_reduce<<<red_blocks, 256, 0, st>>>(nsys, W.cg, W.partial, kPB, 2, tol * tol,
                                                max_iter, 0, 0);
@@ -804,7 +813,7 @@ cudaError_t pcg_solve2(Chp2d* cx, const chp_grid& g, int nsys, double a, double 
     }
   }
   // x = S x^ = sigma T'_i T'_j X -> W.Yv (external layout)
-  k_pcg2_rows<N><<<rg, G2::THREADS, sm, st>>>(p, p.X, p.Y, 0);
+  k_pcg2_rows<N, 0><<<rg, G2::THREADS, sm, st>>>(p, p.X, p.Y, 0);
   k_pcg2_cols<N, 2><<<cgd, G2::THREADS, sm, st>>>(p, p.Y, W.Yv, 0);
   return cudaGetLastError();
 }

@@ -110,27 +110,68 @@ __global__ void k_pcg2_prep(Pcg2 a) {
   }
 }
 
-// rows: out = T'_j in (PI -> PI)
-template <int N>
+// rows (PI -> PI): OP 0: out = T'_j in
+//   OP 1 (E3 fused): P = M^-1 R (+ beta P) formed while the row pair is loaded, out = T'_j P
+//   OP 2 (E1 fused): out = Dk .* P + T'_j in, block partial of P . out into partial[sys * RBLK + block]
+// The fused forms save one pass over P (OP 1) and one write + read of Y (OP 2) per CG iteration.
+// Their elementwise loads are issued kRU elements at a time ahead of the stores: element by
+// element every store may alias the next element's loads and each element then costs one
+// memory round trip (the fused kernels of round 1 ran 556 + 362 us per iteration that way).
+#ifndef CHP_PCG2_FUSE
+#define CHP_PCG2_FUSE 1
+#endif
+template <int N, int OP>
 __global__ void __launch_bounds__(128, 2) k_pcg2_rows(Pcg2 a, const double* in, double* out, int loop) {
   using F = fdst::FG<N>;
   using G2 = Pcg2G<N>;
   constexpr int L = F::L, R = F::R, Q = F::Q;
+  constexpr int kRU = R < 8 ? R : 8;
   extern __shared__ __align__(16) double2 smp[];
+  __shared__ double wpart[G2::GPB];
   const int sys = blockIdx.y;
-  if (pcg2_skip(a.cg[sys], loop)) return;
+  const CgSys& q = a.cg[sys];
+  if (pcg2_skip(q, loop)) return;
   const long long NN = (long long)N * N;
   const int g = threadIdx.x / L, l = threadIdx.x % L;
   const int s = blockIdx.x * G2::GPB + g;
   const bool have = s < N / 2;
-  const long long base = (long long)sys * (NN / 2) + (long long)(have ? s : 0) * N;   // double2
+  const long long row = (long long)(have ? s : 0) * N;
+  const long long base = (long long)sys * (NN / 2) + row;   // double2
   double2* reg = smp + G2::RBASE(g);
   const double2 ac = __ldg(&a.wtab[l]);
   const double2* twl = a.wtab + N + l;
-  const double2* src = reinterpret_cast<const double2*>(in) + base;
+  if (OP == 1) {
+    const double2* Rr = reinterpret_cast<const double2*>(a.R) + base;
+    const double2* Dr = reinterpret_cast<const double2*>(a.Dk) + row;
+    double2* Pr = reinterpret_cast<double2*>(a.P) + base;
+    const bool first = q.iters == 0;
+    const double beta = q.beta, acb = q.acbar;
+#pragma unroll 1
+    for (int i0 = 0; i0 < R; i0 += kRU) {
+      double2 rv[kRU], dv[kRU], pv[kRU];
+#pragma unroll
+      for (int u = 0; u < kRU; ++u) {
+        const int n = l + L * (i0 + u);
+        rv[u] = Rr[n];
+        dv[u] = Dr[n];
+        if (!first) pv[u] = Pr[n];
+      }
+#pragma unroll
+      for (int u = 0; u < kRU; ++u) {
+        const int i = i0 + u, n = l + L * i;
+        const double2 mi = pcg2_mi(dv[u], acb);
+        double2 pn = make_double2(rv[u].x * mi.x, rv[u].y * mi.y);
+        if (!first) pn = make_double2(fma(beta, pv[u].x, pn.x), fma(beta, pv[u].y, pn.y));
+        if (have) Pr[n] = pn;
+        reg[n + i / Q] = pn;
+      }
+    }
+  } else {
+    const double2* src = reinterpret_cast<const double2*>(in) + base;
 #pragma unroll 8
-  for (int i = 0; i < R; ++i) linb::cp16(&reg[l + L * i + i / Q], &src[l + L * i]);
-  linb::cp_wait();
+    for (int i = 0; i < R; ++i) linb::cp16(&reg[l + L * i + i / Q], &src[l + L * i]);
+    linb::cp_wait();
+  }
   __syncwarp();
   double2* ob = fdst::out_base<N>(reg, l);
   fdst::pair_dst<N>(reg, reg, twl, l, 2.0 * ac.y, 2.0 * ac.x,
@@ -139,8 +180,42 @@ __global__ void __launch_bounds__(128, 2) k_pcg2_rows(Pcg2 a, const double* in, 
                       ob[2 * j + 1] = make_double2(a1, b1);
                     });
   __syncwarp();
-  if (have) {
-    double2* dst = reinterpret_cast<double2*>(out) + base;
+  double2* dst = reinterpret_cast<double2*>(out) + base;
+  if (OP == 2) {
+    const double2* Pr = reinterpret_cast<const double2*>(a.P) + base;
+    const double2* Dr = reinterpret_cast<const double2*>(a.Dk) + row;
+    double part = 0.0;
+#pragma unroll 1
+    for (int i0 = 0; i0 < R; i0 += kRU) {
+      double2 pv[kRU], dv[kRU];
+#pragma unroll
+      for (int u = 0; u < kRU; ++u) {
+        const int n = l + L * (i0 + u);
+        pv[u] = Pr[n];
+        dv[u] = Dr[n];
+      }
+#pragma unroll
+      for (int u = 0; u < kRU; ++u) {
+        const int i = i0 + u, n = l + L * i;
+        const double2 y = reg[n + i / Q];
+        const double2 w = make_double2(fma(dv[u].x, pv[u].x, y.x), fma(dv[u].y, pv[u].y, y.y));
+        if (have) {
+          dst[n] = w;
+          part = fma(pv[u].x, w.x, part);
+          part = fma(pv[u].y, w.y, part);
+        }
+      }
+    }
+    // fixed-order block partial: lanes of the group (xor butterfly), then the groups in order
+    for (int o = L / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o, L);
+    if (l == 0) wpart[g] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int k = 0; k < G2::GPB; ++k) t += wpart[k];
+      a.partial[(long long)sys * G2::RBLK + blockIdx.x] = t;
+    }
+  } else if (have) {
 #pragma unroll 8
     for (int i = 0; i < R; ++i) dst[l + L * i] = reg[l + L * i + i / Q];
   }
