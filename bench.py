@@ -291,7 +291,7 @@ def run_gpu(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                      "peak_source": src,
-                     "kernel": "LINEAR_B fine propagator (linb::k2d_rowb + linb::k2d_colb), "
+                     "kernel": "LINEAR_B fine propagator (linb::k2d_rowb + linb::k2d_colt), "
                                "32 B/grid-point-step", "traffic": traffic,
                      "traffic_unit": "DRAM bytes per grid-point-step (ncu, row+column pass)"},
         "coarse_cg_per_step": coarse_cg,
