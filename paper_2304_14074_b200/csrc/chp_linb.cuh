@@ -49,6 +49,15 @@
 
 namespace linb {
 
+// N = 1024 strip length.  Every block runs ceil((SP + 1) / G) chunks whatever its strip holds,
+// so what counts is strips x chunks per field: 63 gives 9 x 16 = 144 chunk slots for the 512 + 9
+// pairs a field needs (the ninth strip has 8 pairs and ran 13 chunks on zeros); 57 gives nine
+// equal strips of 15 chunks = 135 (-6 %).  Measured per 16 steps of 512 / 256 / 64 slices:
+// 63: 104.4 / 52.4 / 13.5 ms; 57: 100.4 / 50.2 / 12.9; 52: 102.0 / 51.2 / 14.1; 74: 100.0 / 50.7 /
+// 14.6; 86: 100.3 / 50.5 / 14.3; 103: 99.7 / 50.1 / 15.6 (too few blocks for small batches).
+#ifndef CHP_ROW_SP
+#define CHP_ROW_SP 57
+#endif
 template <int N> struct RowG {          // row pass geometry
   using F = fdst::FG<N>;
   static constexpr int L = F::L;
@@ -57,8 +66,9 @@ template <int N> struct RowG {          // row pass geometry
   static constexpr int G = THREADS / L;              // lane groups = row pairs per chunk
   static constexpr int NP = N / 2;                   // row pairs per field
   // phase-1 pairs per strip: a strip of SP pairs transforms SP + 1 pairs in phase 0 in
-  // ceil((SP + 1) / G) chunks of G, so SP = 63 (64 / G chunks, 1.6 % halo overhead)
-  static constexpr int SP = (NP < 64) ? NP : 63;
+  // ceil((SP + 1) / G) chunks of G (63: 64 / G chunks, 1.6 % halo overhead; N = 1024: see
+  // CHP_ROW_SP above)
+  static constexpr int SP = (NP < 64) ? NP : (N >= 1024 ? CHP_ROW_SP : 63);
   static constexpr int SLOTS = G + 1;
   static constexpr size_t SMEM = sizeof(double2) * (size_t)SLOTS * F::RS;
   static constexpr int MINB = (N >= 1024) ? CHP_ROW_MINB : 3;
@@ -252,7 +262,14 @@ __global__ void __launch_bounds__(RowG<N>::THREADS, RowG<N>::MINB) k2d_rowb(RowA
   else U = a.in + (a.in_index ? (long long)a.in_index[sys] : (long long)sys) * a.in_stride;
 
   double2 xo[R];                                               // the group's own x pair (phase 0 -> 1)
-  for (int t = 0; t < chunks; ++t) {
+  // chunks this strip needs: phase 1 of chunk t covers pairs sp0 + t G - 1 ... sp0 + t G + G - 2,
+  // so a short last strip (NP = 8 x 63 + 8 at N = 1024) stops after (sp1 - sp0) / G + 1 chunks
+  // instead of running the remaining ones on zeros
+#ifndef CHP_ROW_EARLY
+#define CHP_ROW_EARLY 0
+#endif
+  const int nch = CHP_ROW_EARLY ? min(chunks, (sp1 - sp0) / G + 1) : chunks;
+  for (int t = 0; t < nch; ++t) {
     const int p0 = sp0 + t * G;
     // ---- phase 0: slot of pair s0 = p0 + g holds x rows (2 s0, 2 s0 + 1) ----
     {
