@@ -75,7 +75,14 @@ CHP_DEV double div_rn(double x, double d, double r) {
 // is formed from the same values with the same expressions: bit-identical).
 //   load(r)                      -> double2 (y_{r+1} or 0, aux_r or 0)
 //   make(r, ym, y0, yp, aux, e[5], rhs)  row r from y_{r-1}, y_r, y_{r+1}, aux_r
-constexpr int kPD = 8;
+#ifndef CHP_1D_PD
+#define CHP_1D_PD 8
+#endif
+constexpr int kPD = CHP_1D_PD;
+#ifndef CHP_1D_RQ
+#define CHP_1D_RQ 16
+#endif
+constexpr int kRQ = CHP_1D_RQ > 0 ? CHP_1D_RQ : 1;   // residual loop: rows of y / yhat in flight
 
 template <class Load, class Make>
 CHP_DEV int band_lu_forward(int m, Load load, Make make, double* __restrict__ ub, long long ks) {
@@ -352,6 +359,43 @@ CHP_DEV int step_eyre(const G1& g, double d, double b, double tol, int maxit,
     {
       double ym2 = 0.0, ym1 = 0.0, y0 = y[0], yp1 = ld(y, 1, m);
       double cm = 0.0, c0 = chp_cube(y0);
+#if CHP_1D_RQ > 0
+      // y_{i+2} and yhat_i travel kRQ rows ahead of the (sequential) norm accumulation in a
+      // register queue: the yhat rows are interleaved over the systems and always come from
+      // L2, which an unrolled loop alone left exposed once per unrolled group of rows
+      double yq[kRQ], hq[kRQ];
+#pragma unroll
+      for (int q = 0; q < kRQ; ++q) {
+        yq[q] = ld(y, q + 2, m);
+        hq[q] = (q < m) ? yh[(long long)q * ks] : 0.0;
+      }
+      auto row = [&](int i, double yp2, double yhi) {
+        const double cp = (i + 1 < m) ? chp_cube(yp1) : 0.0;
+        const double s0 = (i == 0 || i == m - 1) ? g.s_edge : g.s_main;
+        const double H = ((y0 + b * bilap5(ym2, ym1, y0, yp1, yp2, s0, g)) -
+                          d * lap3(cm, c0, cp, g.c1)) - yhi;
+        ss = ss + H * H;
+        ym2 = ym1; ym1 = y0; y0 = yp1; yp1 = yp2;
+        cm = c0; c0 = cp;
+      };
+      int i0 = 0;
+      for (; i0 + kRQ <= m; i0 += kRQ) {
+        double yc[kRQ], hc[kRQ];
+#pragma unroll
+        for (int q = 0; q < kRQ; ++q) {
+          yc[q] = yq[q];
+          hc[q] = hq[q];
+          yq[q] = ld(y, i0 + q + kRQ + 2, m);
+          hq[q] = (i0 + q + kRQ < m) ? yh[(long long)(i0 + q + kRQ) * ks] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < kRQ; ++q) row(i0 + q, yc[q], hc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kRQ; ++q)
+        if (i0 + q < m) row(i0 + q, yq[q], hq[q]);
+    }
+#else
       #pragma unroll 8
       for (int i = 0; i < m; ++i) {
         const double yp2 = ld(y, i + 2, m);
@@ -364,6 +408,7 @@ CHP_DEV int step_eyre(const G1& g, double d, double b, double tol, int maxit,
         cm = c0; c0 = cp;
       }
     }
+#endif
     const double r = sqrt(g.hd * ss);
     if (hist != nullptr && it < hlen) hist[it] = r;   // StepReport.residual_history
     if (r <= tol) {
