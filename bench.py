@@ -49,7 +49,7 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,power.draw,power.limit")
 
     def __init__(self, index: int):
         self.index = index
@@ -72,7 +72,7 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
+            if len(parts) >= 6:
                 self.rows.append(parts)
 
     def stop(self) -> dict:
@@ -92,9 +92,18 @@ class ClockSampler:
         mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in rows for k in range(4) if r[2 + k] == "Active"})
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        pw = [num(r[6]) for r in rows if len(r) > 7 and num(r[6]) is not None]
+        pl = [num(r[7]) for r in rows if len(r) > 7 and num(r[7]) is not None]
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows),
+                "power_w": float(np.median(pw)) if pw else None,
+                "power_limit_w": max(pl) if pl else None}
 
 
 def count_launches(fn):
