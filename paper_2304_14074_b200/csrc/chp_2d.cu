@@ -1126,10 +1126,20 @@ cudaError_t sweep_n(Chp2d* c, const chp_grid& g, const chp_spec& sp, int mode, i
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2d_coarse2<N>, G2::THREADS,
                                                     G2::SMEM_RES);
-      // one block per SM: enough lane groups for every row pair, and half the
-      // grid-barrier arrivals of two
-      blocks = sms;
+      // One block per SM at most (half the grid-barrier arrivals of two), and for the smaller
+      // grids only twice the blocks the transforms need (N / (2 GPB) row-pair groups, N / TC
+      // column tiles): the others would only take part in the barriers and the elementwise
+      // loops.  Config 3 (N = 256) to tolerance: 148 blocks 1.30 s, 64: 1.18 s, 32: 1.17 s,
+      // 16: 1.22 s.  N = 1024 needs 128 and keeps every SM.  (The dot products' summation
+      // order follows the block count, so results depend on it in the last bits.)
+      const int need = (N / 2 + G2::GPB - 1) / G2::GPB;
+      blocks = 2 * need < 8 ? 8 : 2 * need;
+      if (blocks > sms) blocks = sms;
       res_ok = per >= 1;
+      if (const char* e = getenv("CHP_C2_BLOCKS")) {      // A/B knob
+        const int want = atoi(e);
+        if (want > 0) blocks = want < need ? (need < sms ? need : sms) : (want < sms ? want : sms);
+      }
     }
     const size_t NN = (size_t)N * N;
     const size_t doubles = 10 * NN + 2 + (size_t)fs + 16 * (size_t)blocks + 16;
