@@ -79,6 +79,9 @@ CHP_DEV double div_rn(double x, double d, double r) {
 #define CHP_1D_PD 8
 #endif
 constexpr int kPD = CHP_1D_PD;
+#ifndef CHP_1D_SPECRCP
+#define CHP_1D_SPECRCP 1
+#endif
 #ifndef CHP_1D_RQ
 #define CHP_1D_RQ 16
 #endif
@@ -119,11 +122,20 @@ CHP_DEV int band_lu_forward(int m, Load load, Make make, double* __restrict__ ub
       const int j = j0 + jj;
       if (j >= m) break;
       const int km = min(2, m - 1 - j);
+#if CHP_1D_SPECRCP
+      // the reciprocals of the three pivot candidates start before the pivot is chosen: the
+      // division is the longest link of the row-to-row dependence chain and the comparisons
+      // and the row swap then run beside it instead of in front of it (same value: RN(1/pivot))
+      const double rc0 = 1.0 / W[0][0], rc1 = 1.0 / W[1][0], rc2 = 1.0 / W[2][0];
+#endif
       int jp = 0;
       double amax = fabs(W[0][0]);
       if (km >= 1 && fabs(W[1][0]) > amax) { jp = 1; amax = fabs(W[1][0]); }
       if (km >= 2 && fabs(W[2][0]) > amax) { jp = 2; }
       double piv = (jp == 0) ? W[0][0] : (jp == 1 ? W[1][0] : W[2][0]);
+#if CHP_1D_SPECRCP
+      const double rcpv = (jp == 0) ? rc0 : (jp == 1 ? rc1 : rc2);
+#endif
       if (piv != 0.0) {
         if (jp != 0) {
 #pragma unroll
@@ -137,7 +149,11 @@ CHP_DEV int band_lu_forward(int m, Load load, Make make, double* __restrict__ ub
           if (jp == 1) bb[1] = t; else bb[2] = t;
         }
         if (km > 0) {
+#if CHP_1D_SPECRCP
+          const double rcp = rcpv;                    // DSCAL(km, ONE/AB(KV+1,J))
+#else
           const double rcp = 1.0 / W[0][0];           // DSCAL(km, ONE/AB(KV+1,J))
+#endif
           W[1][0] = W[1][0] * rcp;
           if (km >= 2) W[2][0] = W[2][0] * rcp;
 #pragma unroll
@@ -155,7 +171,11 @@ CHP_DEV int band_lu_forward(int m, Load load, Make make, double* __restrict__ ub
 #pragma unroll
       for (int c = 0; c < 5; ++c) u[c * ks] = W[0][c];
       u[5 * ks] = bb[0];
+#if CHP_1D_SPECRCP
+      u[6 * ks] = rcpv;                             // RN(1/U_jj) for the backward sweep
+#else
       u[6 * ks] = 1.0 / W[0][0];                    // RN(1/U_jj) for the backward sweep
+#endif
       // slide the window one row/column down; row r = j+3 enters from the queue
 #pragma unroll
       for (int c = 0; c < 4; ++c) { W[0][c] = W[1][c + 1]; W[1][c] = W[2][c + 1]; }
